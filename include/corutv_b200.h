@@ -1,0 +1,124 @@
+/*
+ * corutv_b200.h — C-ABI of the B200-native (sm_100a) CoR-UTV / ALM-CoRUTV
+ * hot path.  Plain pointers and sizes only; all matrices are row-major
+ * (C-order) float64, exactly as the reference's numpy arrays
+ * (/root/reference/pkg/src/corutv/dense.py:4-7).  Matrix pointers are DEVICE
+ * pointers unless the parameter name ends in `_host`; every call is
+ * asynchronous on the handle's stream unless it returns a host scalar.
+ *
+ * Each entry point names the reference interface it replaces
+ * (file:line under /root/reference/pkg/src/corutv/).  The Python host layer
+ * (paper_1906_04572_b200/) binds these with ctypes; INTEGRATION.md shows the
+ * binding a maintainer adds on the reference side.
+ */
+#ifndef CORUTV_B200_H
+#define CORUTV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes (the Python shim maps them to the reference's exceptions). */
+enum corutv_status {
+  CORUTV_OK = 0,
+  CORUTV_ERR_SHAPE = 1,      /* ValueError: "rows >= cols", "exceeds", bad dims (sketch.py:93-98,192-193) */
+  CORUTV_ERR_NONFINITE = 2,  /* ValueError: "contains non-finite entries" (dense.py:48-49) */
+  CORUTV_ERR_CUDA = 3,       /* CUDA runtime/launch failure (CorutvError) */
+  CORUTV_ERR_COMM = 4,       /* collective failure in the row-sharded path (CorutvError) */
+  CORUTV_ERR_CONVERGENCE = 5,/* iteration cap hit (ConvergenceError, errors.py:8-18) */
+  CORUTV_ERR_ARG = 6,        /* invalid argument (ValueError) */
+  CORUTV_ERR_NOMEM = 7       /* device allocation failed (CorutvError) */
+};
+
+enum corutv_variant { CORUTV_EXACT_D = 0, CORUTV_APPROX_D = 1 }; /* sketch.py:52-55 */
+
+typedef struct corutv_handle corutv_handle;
+
+/* Sum-allreduce of `count` float64 values in place on `stream`; returns 0 on
+ * success.  Installed for the row-sharded (multi-GPU) path: the host binds it
+ * to NCCL (torch.distributed) or to any transport.  NULL = single GPU. */
+typedef int (*corutv_allreduce_fn)(void* user, double* buf, int64_t count, void* stream);
+
+/* Library / device handle: owns a growable device workspace and the stream
+ * (a cudaStream_t, or NULL for the legacy default stream). */
+int corutv_create(int device, void* stream, corutv_handle** out);
+void corutv_destroy(corutv_handle* h);
+int corutv_set_stream(corutv_handle* h, void* stream);
+const char* corutv_last_error(const corutv_handle* h);
+int corutv_version(void);
+
+/* Row-sharded mode: this rank owns `m_local` consecutive rows of the global
+ * matrix; sketches over the column space are combined with `fn`
+ * (SURVEY §8e).  world == 1 (or fn == NULL) restores single-GPU mode. */
+int corutv_set_comm(corutv_handle* h, corutv_allreduce_fn fn, void* user, int rank, int world);
+
+/* CoR-UTV: replaces corutv(a, cfg, counter) — sketch.py:182-208, including
+ * _power_sketch (sketch.py:166-179), householder_qr of both sketches
+ * (dense.py:132-149; here a backward-stable adaptive shifted CholeskyQR),
+ * compression (sketch.py:155-158 exact-d / sketch.py:203 approx-d), qrcp
+ * (dense.py:152-192) and the lift (sketch.py:205-207).
+ *   a      : m x n, leading dimension lda (in the sharded mode: the local
+ *            m x n row block; the global row count is the sum over ranks)
+ *   omega  : n x ell Gaussian test matrix (gaussian_matrix, sketch.py:63-68)
+ *   u      : m x ell (ld ell)    t : ell x ell upper triangular (ld ell)
+ *   v      : n x ell (ld ell)    perm : ell int64 (nullable)
+ *   passes_host : incremented by the number of data sweeps (PassCounter,
+ *                 sketch.py:126-163): 2q+3 exact-d, 2q+2 approx-d (nullable)
+ * Synchronises the stream before returning (status depends on device flags). */
+int corutv_decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda,
+                     int ell, int q_power, int variant, const double* omega, double* u, double* t,
+                     double* v, int64_t* perm, int64_t* passes_host);
+
+/* Fused ALM update, rpca.py:211-216 with L = U[:, :r] (T[:r,:] V')
+ * (rpca.py:129) formed tile-by-tile and never stored:
+ *   g  = (M - L) + Y/mu ;  S = sign(g) max(|g| - lam/mu, 0)
+ *   Z  = (M - L) - S    ;  Y <- Y + mu Z
+ *   G' = (M - S) + Y/mu_next   (the next iteration's input, rpca.py:208)
+ * and returns zeta2 = sum Z^2 and nnz = #(|S| > 1e-12) (rpca.py:215-216).
+ * m_mat, s, y, g_next: rows x cols (ld cols); u: rows x ell (ld ell);
+ * t: ell x ell; v: cols x ell.  r in [0, ell]. */
+int corutv_alm_update(corutv_handle* h, const double* m_mat, double* s, double* y, double* g_next,
+                      int64_t rows, int64_t cols, const double* u, const double* t,
+                      const double* v, int ell, int r, double mu, double lam_over_mu,
+                      double mu_next, double* zeta2_host, int64_t* nnz_host);
+
+/* L = U[:, :r] (T[:r, :] V')  — rpca.py:122-132 (_truncate_utv), written out. */
+int corutv_lowrank(corutv_handle* h, const double* u, const double* t, const double* v,
+                   int64_t rows, int64_t cols, int ell, int r, double* l_out);
+
+/* |A|_2 by block power iteration — dense.py:405-442 (b = min(24, n),
+ * disjoint-support start, stop when |est - prev| <= 0.02 tol est).
+ * Matrices with min(m, n) <= 64 use the one-sided Jacobi path
+ * (dense.py:414-415). */
+int corutv_spectral_norm(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda,
+                         double tol, int max_iter, double* out_host, int* iters_host);
+
+/* Singular values (descending) of a small m x n matrix — dense.py:379-387
+ * (one-sided Jacobi, tol 1e-14, <= 100 sweeps).  sig: min(m,n) doubles. */
+int corutv_singular_values(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda,
+                           double* sig);
+
+/* sum of squares of an m x n matrix (rpca.py:187, dense.py:94-96). */
+int corutv_sumsq(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda,
+                 double* out_host);
+
+/* |A - U T V'|_F without materialising U T V' — sketch.py:211-217 (K11). */
+int corutv_lowrank_error(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda,
+                         const double* u, const double* t, const double* v, int ell,
+                         double* out_host);
+
+/* Dense FP64 tensor-core GEMM primitives (the sketch contractions):
+ *   trans_a == 0 : C(M x N) = A(M x K) B(K x N)          — sketch.py:149
+ *   trans_a == 1 : C(M x N) = A(K x M)' B(K x N)         — sketch.py:153
+ * B is K x N (ld ldb).  C has leading dimension ldc. */
+int corutv_gemm(corutv_handle* h, int trans_a, int64_t M, int64_t N, int64_t K, const double* a,
+                int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CORUTV_B200_H */

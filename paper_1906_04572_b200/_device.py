@@ -1,0 +1,79 @@
+"""Host <-> device marshalling shared by the API modules.
+
+Inputs may be numpy-compatible host arrays (copied to the current CUDA
+device) or torch CUDA tensors (used in place, zero-copy when float64 and
+C-contiguous).  Outputs follow the input's residency, like the reference's
+pure functions return fresh numpy arrays (dense.py:4-7).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from ._lib import DeviceUnavailable
+
+
+def torch_mod():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise DeviceUnavailable("no CUDA device: the CoR-UTV B200 path has no CPU fallback")
+    return torch
+
+
+def is_device_tensor(x) -> bool:
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def shape_check(x, name):
+    """The structural part of as_matrix (dense.py:41-47); finiteness is
+    checked on the device."""
+    if is_device_tensor(x):
+        shape = tuple(x.shape)
+    else:
+        x = np.asarray(x, dtype=float)
+        shape = x.shape
+    if len(shape) != 2:
+        raise ValueError(f"{name} must be 2-D, got shape {shape}")
+    if shape[0] < 1 or shape[1] < 1:
+        raise ValueError(f"{name} must have positive dimensions, got {shape}")
+    return x
+
+
+def to_device(x, name="matrix", pin=False):
+    """Return (device float64 tensor with unit inner stride, was_host)."""
+    torch = torch_mod()
+    x = shape_check(x, name)
+    if is_device_tensor(x):
+        t = x
+        if t.dtype != torch.float64:
+            t = t.to(torch.float64)
+        if t.stride(1) != 1 or t.stride(0) < t.shape[1]:
+            t = t.contiguous()
+        return t, False
+    host = np.ascontiguousarray(x, dtype=np.float64)
+    src = torch.from_numpy(host)
+    if pin:
+        src = src.pin_memory()
+    return src.to(torch.cuda.current_device(), non_blocking=pin), True
+
+
+def to_output(t, was_host):
+    if was_host:
+        return t.cpu().numpy()
+    return t
+
+
+def ptr(t) -> int:
+    return t.data_ptr()
+
+
+def raise_if_nonfinite(t, name):
+    """Error-path only: reproduce as_matrix's finiteness message."""
+    torch = torch_mod()
+    if not bool(torch.isfinite(t).all()):
+        raise ValueError(f"{name} contains non-finite entries")

@@ -1,0 +1,973 @@
+// corutv_b200.cu — host orchestration and C-ABI of the B200-native CoR-UTV /
+// ALM-CoRUTV hot path (declarations: include/corutv_b200.h).
+//
+// Everything below runs on one CUDA stream per handle.  Device memory comes
+// from a growable per-handle arena; host-visible scalars go through a small
+// pinned buffer.  The only host synchronisations are the data-dependent
+// decisions the reference also takes on the host (QR step acceptance, the
+// ALM residual / rank counts, the power-iteration stop test).
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "aux.cuh"
+#include "common.cuh"
+#include "gemm.cuh"
+#include "small.cuh"
+
+#define CORUTV_VERSION 100
+
+struct corutv_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  corutv_allreduce_fn ar_fn = nullptr;
+  void* ar_user = nullptr;
+  int rank = 0, world = 1;
+  char* arena = nullptr;
+  size_t arena_size = 0;
+  double* pinned = nullptr;  // 64 doubles of pinned host scratch
+  int num_sms = 148;
+};
+
+namespace {
+
+constexpr double kUnit = 1.1102230246251565e-16;  // 2^-53
+constexpr double kKappaPlain = 1e6;               // accept an unshifted CholQR step below this
+constexpr int kMaxQrSteps = 12;
+
+struct Fail {
+  int code;
+};
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+#define CK(call)                                                                  \
+  do {                                                                            \
+    cudaError_t e_ = (call);                                                      \
+    if (e_ != cudaSuccess) {                                                      \
+      h->err = std::string(#call) + ": " + cudaGetErrorString(e_);                \
+      throw Fail{CORUTV_ERR_CUDA};                                                \
+    }                                                                             \
+  } while (0)
+
+#define CK_LAUNCH()                                                               \
+  do {                                                                            \
+    cudaError_t e_ = cudaGetLastError();                                          \
+    if (e_ != cudaSuccess) {                                                      \
+      h->err = std::string("kernel launch: ") + cudaGetErrorString(e_);           \
+      throw Fail{CORUTV_ERR_CUDA};                                                \
+    }                                                                             \
+  } while (0)
+
+void fail(corutv_handle* h, int code, const std::string& msg) {
+  h->err = msg;
+  throw Fail{code};
+}
+
+// ------------------------------------------------------------------ arena
+struct Arena {
+  corutv_handle* h;
+  size_t off = 0;
+  std::vector<std::pair<void**, size_t>> reqs;
+  template <typename T>
+  void add(T** p, size_t count) {
+    reqs.push_back({reinterpret_cast<void**>(p), round_up(count * sizeof(T), 256)});
+  }
+  void commit() {
+    size_t total = 0;
+    for (auto& r : reqs) total += r.second;
+    if (total > h->arena_size) {
+      if (h->arena) {
+        cudaStreamSynchronize(h->stream);
+        cudaFree(h->arena);
+        h->arena = nullptr;
+        h->arena_size = 0;
+      }
+      size_t want = std::max(total, (size_t)64 << 20);
+      if (cudaMalloc(&h->arena, want) != cudaSuccess) {
+        cudaGetLastError();
+        fail(h, CORUTV_ERR_NOMEM, "device workspace allocation of " + std::to_string(want) + " bytes failed");
+      }
+      h->arena_size = want;
+    }
+    size_t o = 0;
+    for (auto& r : reqs) {
+      *r.first = h->arena + o;
+      o += r.second;
+    }
+  }
+};
+
+// ------------------------------------------------------------ tensor maps
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                      const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                      const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                      CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled_t encode_fn(corutv_handle* h) {
+  static PFN_encodeTiled_t fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+  });
+  if (!fn) fail(h, CORUTV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// 2-D row-major FP64 tensor: `inner` contiguous elements per row, `outer`
+// rows, leading dimension `ld` (elements).  Box {16, box_outer}, 128-B swizzle.
+CUtensorMap make_map(corutv_handle* h, const double* base, int64_t inner, int64_t outer, int64_t ld,
+                     int box_outer) {
+  CUtensorMap m;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld & 1))
+    fail(h, CORUTV_ERR_ARG, "TMA operand must be 16-byte aligned with an even leading dimension");
+  cuuint64_t dims[2] = {(cuuint64_t)std::max<int64_t>(inner, 1), (cuuint64_t)std::max<int64_t>(outer, 1)};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 8)};
+  cuuint32_t box[2] = {16, (cuuint32_t)box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn(h)(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(h, CORUTV_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+// ------------------------------------------------------------------- GEMM
+struct GemmPlan {
+  int J, n_tiles, m_tiles, k_tiles, splits, kps;
+};
+
+GemmPlan plan_gemm(const corutv_handle* h, int64_t M, int64_t N, int64_t K, bool allow_split) {
+  GemmPlan p;
+  p.n_tiles = (int)((N + 127) / 128);
+  p.J = (int)std::min<int64_t>(8, std::max<int64_t>(1, (N + 16 * p.n_tiles - 1) / (16 * p.n_tiles)));
+  p.m_tiles = (int)((M + gemm::BM - 1) / gemm::BM);
+  p.k_tiles = (int)((K + gemm::BK - 1) / gemm::BK);
+  const int64_t base = (int64_t)p.m_tiles * p.n_tiles;
+  const int sms = h->num_sms;
+  int best = 1;
+  double best_cost = 1e300;
+  const int smax = allow_split ? std::min(64, std::max(1, p.k_tiles / 4)) : 1;
+  for (int s = 1; s <= smax; ++s) {
+    const int kps = (p.k_tiles + s - 1) / s;
+    const int sa = (p.k_tiles + kps - 1) / kps;
+    const double waves = std::ceil((double)(base * sa) / sms);
+    // per-split finalisation traffic, in k-tile-equivalents (rough)
+    const double cost = waves * (kps + 4.0) + (sa > 1 ? 0.02 * sa * (double)M * N / (sms * 2048.0) : 0.0);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = sa;
+    }
+  }
+  p.kps = (p.k_tiles + best - 1) / best;
+  p.splits = (p.k_tiles + p.kps - 1) / p.kps;
+  if (p.k_tiles == 0) { p.kps = 0; p.splits = 1; }
+  return p;
+}
+
+template <int J, bool MM, bool CHECK>
+void launch_gemm_t(corutv_handle* h, const CUtensorMap& ma, const CUtensorMap& mb, const gemm::Tile& t,
+                   const gemm::StoreParams& sp, int grid) {
+  auto kern = gemm::gemm_kernel<J, MM, CHECK>;
+  static bool configured = false;
+  if (!configured) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::smem_bytes(J)));
+    configured = true;
+  }
+  kern<<<grid, gemm::THREADS, gemm::smem_bytes(J), h->stream>>>(ma, mb, t, sp);
+  CK_LAUNCH();
+}
+
+template <bool MM, bool CHECK>
+void launch_gemm_j(corutv_handle* h, int J, const CUtensorMap& ma, const CUtensorMap& mb,
+                   const gemm::Tile& t, const gemm::StoreParams& sp, int grid) {
+  switch (J) {
+    case 1: launch_gemm_t<1, MM, CHECK>(h, ma, mb, t, sp, grid); break;
+    case 2: launch_gemm_t<2, MM, CHECK>(h, ma, mb, t, sp, grid); break;
+    case 3: launch_gemm_t<3, MM, CHECK>(h, ma, mb, t, sp, grid); break;
+    case 4: launch_gemm_t<4, MM, CHECK>(h, ma, mb, t, sp, grid); break;
+    case 5: launch_gemm_t<5, MM, CHECK>(h, ma, mb, t, sp, grid); break;
+    case 6: launch_gemm_t<6, MM, CHECK>(h, ma, mb, t, sp, grid); break;
+    case 7: launch_gemm_t<7, MM, CHECK>(h, ma, mb, t, sp, grid); break;
+    default: launch_gemm_t<8, MM, CHECK>(h, ma, mb, t, sp, grid); break;
+  }
+}
+
+void launch_grid_1d(int64_t total, int* blocks, int* threads) {
+  *threads = 256;
+  *blocks = (int)std::min<int64_t>(std::max<int64_t>(1, (total + 255) / 256), 148 * 16);
+}
+
+void zero2d(corutv_handle* h, double* p, int64_t rows, int64_t cols, int64_t ld) {
+  int nb, tb;
+  launch_grid_1d(rows * cols, &nb, &tb);
+  aux::fill2d_kernel<<<nb, tb, 0, h->stream>>>(p, rows, cols, ld, 0.0);
+  CK_LAUNCH();
+}
+
+// Workspace needed by gemm() for split-K partials.
+size_t gemm_ws_elems(const corutv_handle* h, int64_t M, int64_t N, int64_t K) {
+  GemmPlan p = plan_gemm(h, M, N, K, true);
+  const int64_t ldw = round_up(N, 2);
+  return (size_t)(p.splits > 1 ? p.splits * M * ldw : 0) + (size_t)M * ldw /* transposed path */;
+}
+
+// mm == false: C = A (M x K, lda) * Bt^T, Bt: N x K (ldb)
+// mm == true : C = A^T * B, A: K x M (lda), B: K x N (ldb)
+// C (M x N, ldc) and/or Ct (N x M, ldct).  ws: split-K partial scratch.
+void run_gemm(corutv_handle* h, bool mm, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+          const double* B, int64_t ldb, double* C, int64_t ldc, double* Ct, int64_t ldct, double* ws,
+          int* bad_flag = nullptr) {
+  if (M <= 0 || N <= 0) return;
+  int tb, nb;
+  if (K <= 0) {
+    if (C) zero2d(h, C, M, N, ldc);
+    if (Ct) zero2d(h, Ct, N, M, ldct);
+    return;
+  }
+  GemmPlan p = plan_gemm(h, M, N, K, true);
+  gemm::Tile t;
+  t.M = (int)M;
+  t.N = (int)N;
+  t.K = (int)K;
+  t.m_tiles = p.m_tiles;
+  t.n_tiles = p.n_tiles;
+  t.k_tiles = p.k_tiles;
+  t.k_tiles_per_split = p.kps;
+  t.splits = p.splits;
+  CUtensorMap ma, mb;
+  if (!mm) {
+    ma = make_map(h, A, K, M, lda, gemm::BM);
+    mb = make_map(h, B, K, N, ldb, 16 * p.J);
+  } else {
+    ma = make_map(h, A, M, K, lda, gemm::BK);
+    mb = make_map(h, B, N, K, ldb, gemm::BK);
+  }
+  const bool direct = (p.splits == 1 && Ct == nullptr && C != nullptr);
+  const int64_t ldw = round_up(N, 2);
+  gemm::StoreParams sp;
+  sp.bad_flag = bad_flag;
+  if (direct) {
+    sp.c = C;
+    sp.ldc = ldc;
+    sp.split_stride = 0;
+  } else {
+    sp.c = ws;
+    sp.ldc = ldw;
+    sp.split_stride = M * ldw;
+  }
+  const int grid = p.m_tiles * p.n_tiles * p.splits;
+  if (mm) {
+    if (bad_flag) launch_gemm_j<true, true>(h, p.J, ma, mb, t, sp, grid);
+    else launch_gemm_j<true, false>(h, p.J, ma, mb, t, sp, grid);
+  } else {
+    if (bad_flag) launch_gemm_j<false, true>(h, p.J, ma, mb, t, sp, grid);
+    else launch_gemm_j<false, false>(h, p.J, ma, mb, t, sp, grid);
+  }
+  if (!direct) {
+    launch_grid_1d(M * N, &nb, &tb);
+    aux::splitk_finalize_kernel<<<nb, tb, 0, h->stream>>>(ws, p.splits, M * ldw, M, N, ldw, C, ldc, Ct, ldct);
+    CK_LAUNCH();
+  }
+}
+
+void transpose(corutv_handle* h, const double* src, int64_t rows, int64_t cols, int64_t lds, double* dst,
+               int64_t ldd) {
+  if (rows <= 0 || cols <= 0) return;
+  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  aux::transpose_kernel<<<grid, dim3(32, 8), 0, h->stream>>>(src, rows, cols, lds, dst, ldd);
+  CK_LAUNCH();
+}
+
+void copy2d(corutv_handle* h, const double* src, int64_t rows, int64_t cols, int64_t lds, double* dst,
+            int64_t ldd) {
+  int nb, tb;
+  launch_grid_1d(rows * cols, &nb, &tb);
+  aux::copy2d_kernel<<<nb, tb, 0, h->stream>>>(src, rows, cols, lds, dst, ldd);
+  CK_LAUNCH();
+}
+
+void allreduce(corutv_handle* h, double* buf, int64_t count) {
+  if (h->world <= 1 || !h->ar_fn) return;
+  if (h->ar_fn(h->ar_user, buf, count, (void*)h->stream) != 0)
+    fail(h, CORUTV_ERR_COMM, "allreduce callback failed");
+}
+
+void sync(corutv_handle* h) { CK(cudaStreamSynchronize(h->stream)); }
+
+double global_rows(corutv_handle* h, int64_t m_local) {
+  if (h->world <= 1 || !h->ar_fn) return (double)m_local;
+  h->pinned[0] = (double)m_local;
+  // route through a device scalar so the callback sees device memory
+  double* d;
+  CK(cudaMallocAsync(&d, sizeof(double), h->stream));
+  CK(cudaMemcpyAsync(d, h->pinned, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  allreduce(h, d, 1);
+  CK(cudaMemcpyAsync(h->pinned, d, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaFreeAsync(d, h->stream));
+  sync(h);
+  return h->pinned[0];
+}
+
+// ----------------------------------------------------- small-kernel launch
+int max_optin_smem(corutv_handle* h) {
+  int v = 0;
+  CK(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+  return v;
+}
+
+template <typename K>
+void set_smem(corutv_handle* h, K kern, size_t bytes) {
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+// ------------------------------------------------ adaptive CholeskyQR
+// In place of householder_qr(...).q (dense.py:132-149): returns the buffer
+// (xa or xb) that holds Q.  X has `rows` local rows (ld ldx), ell columns.
+struct QrWork {
+  double* G;      // ell x ldx
+  double* rinvT;  // ell x ldx
+  double* gwork;  // ell * ell
+  double* ws;     // split-K scratch
+  small::CholInfo* info;  // device
+};
+
+double* cholqr(corutv_handle* h, double* xa, double* xb, int64_t rows, int ell, int64_t ldx,
+               double rows_global, bool sharded, const QrWork& w, int* steps_out = nullptr) {
+  const int l = ell;
+  const double coeff = 11.0 * (rows_global * l + (double)l * (l + 1)) * kUnit;
+  const size_t wbytes = (size_t)l * l * 8;
+  const int optin = max_optin_smem(h);
+  const bool smem = wbytes + 8 * 1024 <= (size_t)optin - 8 * 1024;
+  if (smem) set_smem(h, small::chol_factor_kernel, wbytes);
+  double* cur = xa;
+  double* nxt = xb;
+  int plain = 0;
+  for (int step = 0; step < kMaxQrSteps; ++step) {
+    run_gemm(h, true, l, l, rows, cur, ldx, cur, ldx, w.G, ldx, nullptr, 0, w.ws);
+    if (sharded) allreduce(h, w.G, (int64_t)l * ldx);
+    small::chol_factor_kernel<<<1, small::THREADS, smem ? wbytes : 0, h->stream>>>(
+        w.G, l, ldx, coeff, 1, kKappaPlain, w.rinvT, ldx, w.gwork, smem ? 1 : 0, w.info);
+    CK_LAUNCH();
+    run_gemm(h, false, rows, l, l, cur, ldx, w.rinvT, ldx, nxt, ldx, nullptr, 0, w.ws);
+    std::swap(cur, nxt);
+    CK(cudaMemcpyAsync(h->pinned, w.info, sizeof(small::CholInfo), cudaMemcpyDeviceToHost, h->stream));
+    sync(h);
+    small::CholInfo info;
+    std::memcpy(&info, h->pinned, sizeof(info));
+    if (info.status == 2) fail(h, CORUTV_ERR_NONFINITE, "sketch contains non-finite entries");
+    if (info.status == 1) {
+      if (steps_out) *steps_out = step + 1;
+      return cur;
+    }
+    plain = info.shifted ? 0 : plain + 1;
+    if (plain == 2) {
+      if (steps_out) *steps_out = step + 1;
+      return cur;
+    }
+  }
+  fail(h, CORUTV_ERR_CONVERGENCE, "CholeskyQR did not reach orthogonality");
+  return nullptr;
+}
+
+// --------------------------------------------------------------- QRCP
+void qrcp(corutv_handle* h, const double* D, int l, int64_t ldd, double* T, int64_t ldt, double* qtT,
+          int64_t ldq, long long* perm_out, int* perm32, double* gwork) {
+  const int optin = max_optin_smem(h);
+  const size_t stat = 6 * small::LMAX * 8 + 1024;
+  const size_t one = (size_t)l * l * 8;
+  int smR = 0, smQ = 0;
+  size_t dyn = 0;
+  if (2 * one + stat <= (size_t)optin) {
+    smR = smQ = 1;
+    dyn = 2 * one;
+  } else if (one + stat <= (size_t)optin) {
+    smR = 1;
+    dyn = one;
+  }
+  if (dyn) set_smem(h, small::qrcp_kernel, dyn);
+  small::qrcp_kernel<<<1, small::THREADS, dyn, h->stream>>>(D, l, ldd, T, ldt, qtT, ldq, perm_out, perm32,
+                                                            gwork, smR, smQ);
+  CK_LAUNCH();
+}
+
+// one-sided Jacobi: singular values of the matrix whose columns are the nv
+// rows of X (len each); optional pinv.  gwork: (n+1)*(len+n) doubles.
+void jacobi(corutv_handle* h, const double* X, int nv, int len, int64_t ldx, double* sig, double* pinv,
+            int64_t ldp, double* gwork, int* status) {
+  const int n = nv + (nv > 1 && (nv & 1));
+  const size_t bytes = ((size_t)n * len + (pinv ? (size_t)n * n : 0)) * 8;
+  const int optin = max_optin_smem(h);
+  const size_t stat = (small::LMAX * 2 + small::LMAX) * 8 + 8 * 1024;
+  const bool smem = bytes + stat <= (size_t)optin;
+  if (smem) set_smem(h, small::jacobi_kernel, bytes);
+  small::jacobi_kernel<<<1, small::THREADS, smem ? bytes : 0, h->stream>>>(
+      X, nv, len, ldx, 1e-14, 100, sig, pinv, ldp, gwork, smem ? 1 : 0, status);
+  CK_LAUNCH();
+}
+
+// ------------------------------------------------------------ CoR-UTV
+void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, int ell, int q,
+               int variant, const double* omega, double* u, double* t, double* v, int64_t* perm,
+               int64_t* passes_host) {
+  if (!a || !omega || !u || !t || !v) fail(h, CORUTV_ERR_ARG, "null pointer argument");
+  if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
+  if (ell < 1) fail(h, CORUTV_ERR_ARG, "ell must be >= 1, got " + std::to_string(ell));
+  if (ell > small::LMAX) fail(h, CORUTV_ERR_ARG, "ell above the supported maximum 640");
+  if (q < 0) fail(h, CORUTV_ERR_ARG, "q_power must be >= 0");
+  if (variant != CORUTV_EXACT_D && variant != CORUTV_APPROX_D) fail(h, CORUTV_ERR_ARG, "bad variant");
+  if (lda < n) fail(h, CORUTV_ERR_ARG, "lda < n");
+  const bool sharded = h->world > 1 && h->ar_fn;
+  const double mg = global_rows(h, m);
+  if (mg < (double)n)
+    fail(h, CORUTV_ERR_SHAPE, "corutv requires rows >= cols, got " + std::to_string((long long)mg) + "x" + std::to_string(n));
+  if ((double)ell > std::min(mg, (double)n))
+    fail(h, CORUTV_ERR_SHAPE, "ell=" + std::to_string(ell) + " exceeds min(m, n)=" +
+                                  std::to_string((long long)std::min(mg, (double)n)));
+
+  const int l = ell;
+  const int64_t ldp = round_up(l, 16);
+  const int64_t ldn = round_up(n, 16);
+  const bool a_ok = ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && (lda % 2 == 0);
+  const int64_t ldA = a_ok ? lda : round_up(n, 16);
+
+  Arena ar{h};
+  double *Apad = nullptr, *Xn[2], *XT, *C1a, *C1b, *C2a, *C2b, *P, *G, *rinvT, *D, *qtT, *B1, *B2t, *pinvB;
+  double *gwork, *ws, *sigs;
+  int *flag, *perm32, *jstat;
+  small::CholInfo* info;
+  if (!a_ok) ar.add(&Apad, (size_t)m * ldA);
+  ar.add(&Xn[0], (size_t)n * ldp);
+  ar.add(&Xn[1], (size_t)n * ldp);
+  ar.add(&XT, (size_t)l * ldn);
+  ar.add(&C1a, (size_t)m * ldp);
+  ar.add(&C1b, (size_t)m * ldp);
+  ar.add(&C2a, (size_t)n * ldp);
+  ar.add(&C2b, (size_t)n * ldp);
+  ar.add(&P, (size_t)m * ldp);
+  ar.add(&G, (size_t)ldp * ldp);
+  ar.add(&rinvT, (size_t)ldp * ldp);
+  ar.add(&D, (size_t)ldp * ldp);
+  ar.add(&qtT, (size_t)ldp * ldp);
+  ar.add(&B1, (size_t)ldp * ldp);
+  ar.add(&B2t, (size_t)ldp * ldp);
+  ar.add(&pinvB, (size_t)ldp * ldp);
+  ar.add(&gwork, (size_t)(l + 2) * (2 * l + 4) + 2 * (size_t)l * l + 16);
+  ar.add(&sigs, (size_t)ldp);
+  size_t wse = 0;
+  wse = std::max(wse, gemm_ws_elems(h, m, l, n));
+  wse = std::max(wse, gemm_ws_elems(h, n, l, m));
+  wse = std::max(wse, gemm_ws_elems(h, l, l, m));
+  wse = std::max(wse, gemm_ws_elems(h, l, l, n));
+  ar.add(&ws, wse + 16);
+  ar.add(&flag, 4);
+  ar.add(&perm32, (size_t)ldp);
+  ar.add(&jstat, 4);
+  ar.add(&info, 2);
+  ar.commit();
+
+  const double* A = a;
+  if (!a_ok) {
+    copy2d(h, a, m, n, lda, Apad, ldA);
+    A = Apad;
+  }
+  CK(cudaMemsetAsync(flag, 0, sizeof(int), h->stream));
+  // Omega -> Xn[0] (n x ldp) and X^T (l x ldn)
+  copy2d(h, omega, n, l, l, Xn[0], ldp);
+  transpose(h, omega, n, l, l, XT, ldn);
+
+  // power sketch (sketch.py:166-179): C1 = A X ; C2 = A' C1, q+1 times
+  int cur = 0;
+  for (int it = 0; it <= q; ++it) {
+    run_gemm(h, false, m, l, n, A, ldA, XT, ldn, C1a, ldp, nullptr, 0, ws, it == 0 ? flag : nullptr);
+    if (!sharded) {
+      run_gemm(h, true, n, l, m, A, ldA, C1a, ldp, Xn[cur ^ 1], ldp, it < q ? XT : nullptr, ldn, ws);
+    } else {
+      run_gemm(h, true, n, l, m, A, ldA, C1a, ldp, Xn[cur ^ 1], ldp, nullptr, 0, ws);
+      allreduce(h, Xn[cur ^ 1], n * ldp);
+      if (it < q) transpose(h, Xn[cur ^ 1], n, l, ldp, XT, ldn);
+    }
+    cur ^= 1;
+  }
+  // Xn[cur] = C2 (final), Xn[cur^1] = C2 entering the last C1 product
+  double* c2 = Xn[cur];
+  double* c2_in = Xn[cur ^ 1];
+  if (sharded) {
+    // the non-finite flag must be agreed by all ranks before anything else
+    double* fd = gwork;  // reuse scratch: flag as double
+    CK(cudaMemcpyAsync(h->pinned, flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    sync(h);
+    int fl = *reinterpret_cast<int*>(h->pinned);
+    h->pinned[1] = (double)fl;
+    CK(cudaMemcpyAsync(fd, h->pinned + 1, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    allreduce(h, fd, 1);
+    CK(cudaMemcpyAsync(h->pinned + 1, fd, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    sync(h);
+    if (h->pinned[1] > 0.0) fail(h, CORUTV_ERR_NONFINITE, "a contains non-finite entries");
+  } else {
+    CK(cudaMemcpyAsync(h->pinned, flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    sync(h);
+    if (*reinterpret_cast<int*>(h->pinned)) fail(h, CORUTV_ERR_NONFINITE, "a contains non-finite entries");
+  }
+
+  // orthonormalise both sketches (sketch.py:198-199)
+  QrWork w{G, rinvT, gwork, ws, info};
+  CK(cudaMemcpyAsync(C2a, c2, (size_t)n * ldp * 8, cudaMemcpyDeviceToDevice, h->stream));
+  if (variant == CORUTV_APPROX_D)
+    CK(cudaMemcpyAsync(P, C1a, (size_t)m * ldp * 8, cudaMemcpyDeviceToDevice, h->stream));
+  double* Q1 = cholqr(h, C1a, C1b, m, l, ldp, mg, sharded, w);
+  double* Q2 = cholqr(h, C2a, C2b, n, l, ldp, (double)n, false, w);
+
+  // compressed core (sketch.py:200-203)
+  int64_t passes = 2 * (q + 1);
+  if (variant == CORUTV_EXACT_D) {
+    transpose(h, Q2, n, l, ldp, XT, ldn);
+    run_gemm(h, false, m, l, n, A, ldA, XT, ldn, P, ldp, nullptr, 0, ws);  // P = A Q2
+    run_gemm(h, true, l, l, m, Q1, ldp, P, ldp, D, ldp, nullptr, 0, ws);    // D = Q1' P
+    if (sharded) allreduce(h, D, (int64_t)l * ldp);
+    passes += 1;
+  } else {
+    // D = (Q1' C1) pinv(Q2' C2_in)   (sketch.py:203, dense.py:390-402)
+    run_gemm(h, true, l, l, m, Q1, ldp, P, ldp, B1, ldp, nullptr, 0, ws);       // B1 = Q1' C1
+    if (sharded) allreduce(h, B1, (int64_t)l * ldp);
+    run_gemm(h, true, l, l, n, c2_in, ldp, Q2, ldp, B2t, ldp, nullptr, 0, ws);  // B2' = C2_in' Q2
+    jacobi(h, B2t, l, l, ldp, sigs, pinvB, ldp, gwork, jstat);              // pinv(B2)
+    dim3 g((l + 15) / 16, (l + 15) / 16);
+    aux::small_matmul_kernel<<<g, dim3(16, 16), 0, h->stream>>>(B1, ldp, 0, pinvB, ldp, 0, l, l, l, D, ldp);
+    CK_LAUNCH();
+  }
+  qrcp(h, D, l, ldp, t, l, qtT, ldp, reinterpret_cast<long long*>(perm), perm32, gwork);
+  // lift (sketch.py:205-207)
+  run_gemm(h, false, m, l, l, Q1, ldp, qtT, ldp, u, l, nullptr, 0, ws);
+  {
+    int nb, tb;
+    launch_grid_1d(n * l, &nb, &tb);
+    aux::gather_cols_kernel<<<nb, tb, 0, h->stream>>>(Q2, n, l, ldp, perm32, v, l);
+    CK_LAUNCH();
+  }
+  sync(h);
+  if (passes_host) *passes_host += passes;
+}
+
+
+// --------------------------------------------- low-rank product epilogues
+template <int J, int MODE>
+void launch_lr_t(corutv_handle* h, const CUtensorMap& mu, const CUtensorMap& mw, const gemm::Tile& t,
+                 const gemm::LrParams& p, int grid) {
+  auto kern = gemm::lowrank_kernel<J, MODE>;
+  static bool configured = false;
+  if (!configured) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::smem_bytes(J)));
+    configured = true;
+  }
+  kern<<<grid, gemm::THREADS, gemm::smem_bytes(J), h->stream>>>(mu, mw, t, p);
+  CK_LAUNCH();
+}
+
+template <int MODE>
+void launch_lr(corutv_handle* h, int J, const CUtensorMap& mu, const CUtensorMap& mw, const gemm::Tile& t,
+               const gemm::LrParams& p, int grid) {
+  switch (J) {
+    case 1: launch_lr_t<1, MODE>(h, mu, mw, t, p, grid); break;
+    case 2: launch_lr_t<2, MODE>(h, mu, mw, t, p, grid); break;
+    case 3: launch_lr_t<3, MODE>(h, mu, mw, t, p, grid); break;
+    case 4: launch_lr_t<4, MODE>(h, mu, mw, t, p, grid); break;
+    case 5: launch_lr_t<5, MODE>(h, mu, mw, t, p, grid); break;
+    case 6: launch_lr_t<6, MODE>(h, mu, mw, t, p, grid); break;
+    case 7: launch_lr_t<7, MODE>(h, mu, mw, t, p, grid); break;
+    default: launch_lr_t<8, MODE>(h, mu, mw, t, p, grid); break;
+  }
+}
+
+// out = U[:, :r] (T[:r, :] V') consumed tile by tile by the MODE epilogue.
+// U: rows x ell, T: ell x ell, V: cols x ell (all ld ell, device).
+// Returns (sum, count) for the reducing modes (already all-reduced).
+void lowrank_op(corutv_handle* h, int mode, const double* u, const double* t, const double* v,
+                int64_t rows, int64_t cols, int ell, int r, gemm::LrParams p, double out2[2]) {
+  if (rows < 1 || cols < 1 || ell < 1 || r < 0 || r > ell) fail(h, CORUTV_ERR_ARG, "bad low-rank operand shape");
+  const int64_t ldr = round_up(std::max(r, 1), 16), ldl = round_up(ell, 16);
+  const int n_tiles = (int)((cols + 127) / 128);
+  const int J = (int)std::min<int64_t>(8, std::max<int64_t>(1, (cols + 16 * n_tiles - 1) / (16 * n_tiles)));
+  const int m_tiles = (int)((rows + gemm::BM - 1) / gemm::BM);
+  const int grid = m_tiles * n_tiles;
+  Arena ar{h};
+  double *Up, *Tr, *Vp, *Wt, *ws, *part, *out;
+  long long* cnt;
+  ar.add(&Up, (size_t)rows * ldr);
+  ar.add(&Tr, (size_t)ldr * ldl);
+  ar.add(&Vp, (size_t)cols * ldl);
+  ar.add(&Wt, (size_t)cols * ldr);
+  ar.add(&ws, gemm_ws_elems(h, cols, std::max(r, 1), ell) + 16);
+  ar.add(&part, (size_t)grid);
+  ar.add(&cnt, (size_t)grid);
+  ar.add(&out, 2);
+  ar.commit();
+  gemm::Tile tl;
+  tl.M = (int)rows;
+  tl.N = (int)cols;
+  tl.K = r;
+  tl.m_tiles = m_tiles;
+  tl.n_tiles = n_tiles;
+  tl.k_tiles = (r + gemm::BK - 1) / gemm::BK;
+  tl.k_tiles_per_split = tl.k_tiles;
+  tl.splits = 1;
+  if (r > 0) {
+    copy2d(h, u, rows, r, ell, Up, ldr);
+    copy2d(h, t, r, ell, ell, Tr, ldl);
+    copy2d(h, v, cols, ell, ell, Vp, ldl);
+    // Wt = V T_r'  (= (T_r V')')  — rpca.py:129 "head @ f.v.T"
+    run_gemm(h, false, cols, r, ell, Vp, ldl, Tr, ldl, Wt, ldr, nullptr, 0, ws);
+  }
+  CUtensorMap mu = make_map(h, Up, std::max(r, 1), rows, ldr, gemm::BM);
+  CUtensorMap mw = make_map(h, Wt, std::max(r, 1), cols, ldr, 16 * J);
+  p.part_sum = part;
+  p.part_cnt = cnt;
+  if (mode == gemm::LR_STORE) launch_lr<gemm::LR_STORE>(h, J, mu, mw, tl, p, grid);
+  else if (mode == gemm::LR_ALM) launch_lr<gemm::LR_ALM>(h, J, mu, mw, tl, p, grid);
+  else launch_lr<gemm::LR_RESID>(h, J, mu, mw, tl, p, grid);
+  if (mode != gemm::LR_STORE) {
+    aux::finalize_sums_kernel<<<1, 1024, 0, h->stream>>>(part, mode == gemm::LR_ALM ? cnt : nullptr, grid, out);
+    CK_LAUNCH();
+    if (h->world > 1 && h->ar_fn) allreduce(h, out, 2);
+    CK(cudaMemcpyAsync(h->pinned, out, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    sync(h);
+    out2[0] = h->pinned[0];
+    out2[1] = h->pinned[1];
+  }
+}
+
+double sumsq(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda) {
+  const int blocks = 148 * 8;
+  Arena ar{h};
+  double *part, *out;
+  ar.add(&part, blocks);
+  ar.add(&out, 2);
+  ar.commit();
+  aux::sumsq_partial_kernel<<<blocks, 256, 0, h->stream>>>(a, m, n, lda, part);
+  CK_LAUNCH();
+  aux::finalize_sums_kernel<<<1, 1024, 0, h->stream>>>(part, nullptr, blocks, out);
+  CK_LAUNCH();
+  if (h->world > 1 && h->ar_fn) allreduce(h, out, 2);
+  CK(cudaMemcpyAsync(h->pinned, out, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  sync(h);
+  return h->pinned[0];
+}
+
+// singular values of a small (unsharded) m x n matrix, descending.
+void singular_values(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, double* sig) {
+  if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
+  const int64_t k = std::min(m, n);
+  if (k > small::LMAX) fail(h, CORUTV_ERR_ARG, "singular_values: matrix too large for the small-matrix path");
+  const int64_t len = std::max(m, n);
+  Arena ar{h};
+  double *xt = nullptr, *gw;
+  int* st;
+  if (m >= n) ar.add(&xt, (size_t)n * len);
+  ar.add(&gw, (size_t)(k + 2) * (len + k + 2));
+  ar.add(&st, 4);
+  ar.commit();
+  const double* X = a;
+  int64_t ldx = lda;
+  if (m >= n) {  // vectors = columns of a
+    transpose(h, a, m, n, lda, xt, len);
+    X = xt;
+    ldx = len;
+  }
+  jacobi(h, X, (int)k, (int)len, ldx, sig, nullptr, 0, gw, st);
+  CK(cudaMemcpyAsync(h->pinned, st, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  sync(h);
+  if (*reinterpret_cast<int*>(h->pinned))
+    fail(h, CORUTV_ERR_CONVERGENCE, "one-sided Jacobi did not converge in 100 sweeps");
+}
+
+// |A|_2, dense.py:405-442.
+void spectral_norm(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, double tol,
+                   int max_iter, double* out, int* iters) {
+  if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
+  const bool sharded = h->world > 1 && h->ar_fn;
+  const double mg = global_rows(h, m);
+  if (std::min(mg, (double)n) <= 64) {
+    if (sharded) fail(h, CORUTV_ERR_ARG, "spectral_norm: the Jacobi path is single-GPU only");
+    Arena ar{h};
+    double* sig;
+    ar.add(&sig, 128);
+    ar.commit();
+    singular_values(h, a, m, n, lda, sig);
+    CK(cudaMemcpyAsync(h->pinned, sig, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    sync(h);
+    *out = h->pinned[0];
+    if (iters) *iters = 0;
+    return;
+  }
+  const bool tall = mg >= (double)n;
+  if (!tall && sharded) fail(h, CORUTV_ERR_ARG, "spectral_norm: sharded input must have rows >= cols");
+  const int64_t np = tall ? n : m;   // dimension of v
+  const int64_t mp = tall ? m : n;   // rows of w (local)
+  const int b = (int)std::min<int64_t>(24, np);
+  const int64_t ldb = 16;
+  const int64_t ldnp = round_up(np, 16);
+  const bool a_ok = ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && (lda % 2 == 0);
+  const int64_t ldA = a_ok ? lda : round_up(n, 16);
+  const int64_t ldb2 = round_up(b, 16);
+  Arena ar{h};
+  double *Apad = nullptr, *vT, *v, *w, *wT, *z0, *z1, *G, *sig, *ws, *rinvT, *gwork, *G2;
+  small::CholInfo* info;
+  int* st;
+  if (!a_ok) ar.add(&Apad, (size_t)m * ldA);
+  ar.add(&vT, (size_t)b * ldnp);
+  ar.add(&v, (size_t)np * ldb2);
+  ar.add(&w, (size_t)mp * ldb2);
+  ar.add(&wT, (size_t)b * round_up(mp, 16));
+  ar.add(&z0, (size_t)np * ldb2);
+  ar.add(&z1, (size_t)np * ldb2);
+  ar.add(&G, (size_t)ldb2 * ldb2);
+  ar.add(&G2, (size_t)ldb2 * ldb2);
+  ar.add(&rinvT, (size_t)ldb2 * ldb2);
+  ar.add(&sig, 64);
+  ar.add(&gwork, (size_t)(b + 2) * (4 * b + 8));
+  size_t wse = std::max({gemm_ws_elems(h, m, b, n), gemm_ws_elems(h, n, b, m), gemm_ws_elems(h, b, b, m),
+                         gemm_ws_elems(h, b, b, n)});
+  ar.add(&ws, wse + 16);
+  ar.add(&info, 2);
+  ar.add(&st, 4);
+  ar.commit();
+  (void)ldb;
+  const double* A = a;
+  if (!a_ok) {
+    copy2d(h, a, m, n, lda, Apad, ldA);
+    A = Apad;
+  }
+  int nb, tb;
+  launch_grid_1d(b * np, &nb, &tb);
+  aux::snorm_init_kernel<<<nb, tb, 0, h->stream>>>(vT, b, np, ldnp);
+  CK_LAUNCH();
+  transpose(h, vT, b, np, ldnp, v, ldb2);
+  QrWork qw{G2, rinvT, gwork, ws, info};
+  double prev = 0.0;
+  for (int it = 0; it < max_iter; ++it) {
+    // w = A' v  (A' = A if tall else A^T)
+    if (tall) run_gemm(h, false, m, b, n, A, ldA, vT, ldnp, w, ldb2, nullptr, 0, ws);
+    else run_gemm(h, true, n, b, m, A, ldA, v, ldb2, w, ldb2, nullptr, 0, ws);
+    // est = sigma_1(w) = sqrt(lambda_max(w'w))
+    run_gemm(h, true, b, b, mp, w, ldb2, w, ldb2, G, ldb2, nullptr, 0, ws);
+    if (sharded) allreduce(h, G, (int64_t)b * ldb2);
+    jacobi(h, G, b, b, ldb2, sig, nullptr, 0, gwork, st);
+    CK(cudaMemcpyAsync(h->pinned, sig, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    sync(h);
+    const double est = std::sqrt(std::max(h->pinned[0], 0.0));
+    if (iters) *iters = it + 1;
+    if (est == 0.0) { *out = 0.0; return; }
+    if (std::fabs(est - prev) <= 0.02 * tol * est) { *out = est; return; }
+    prev = est;
+    // v = orth(A'^T w)
+    if (tall) {
+      run_gemm(h, true, n, b, m, A, ldA, w, ldb2, z0, ldb2, nullptr, 0, ws);
+      if (sharded) allreduce(h, z0, n * ldb2);
+    } else {
+      transpose(h, w, n, b, ldb2, wT, round_up(mp, 16));
+      run_gemm(h, false, m, b, n, A, ldA, wT, round_up(mp, 16), z0, ldb2, nullptr, 0, ws);
+    }
+    double* q = cholqr(h, z0, z1, np, b, ldb2, (double)np, false, qw);
+    if (q != v) CK(cudaMemcpyAsync(v, q, (size_t)np * ldb2 * 8, cudaMemcpyDeviceToDevice, h->stream));
+    transpose(h, v, np, b, ldb2, vT, ldnp);
+  }
+  *out = prev;
+  fail(h, CORUTV_ERR_CONVERGENCE, "spectral norm power iteration did not converge");
+}
+
+}  // namespace
+
+// =================================================================== C-ABI
+#define ABI_BEGIN(hh)                                  \
+  corutv_handle* h = (hh);                             \
+  if (!h) return CORUTV_ERR_ARG;                       \
+  h->err.clear();                                      \
+  try {                                                \
+    CK(cudaSetDevice(h->device));
+#define ABI_END                                        \
+  }                                                    \
+  catch (const Fail& f) {                              \
+    return f.code;                                     \
+  }                                                    \
+  return CORUTV_OK;
+
+extern "C" {
+
+int corutv_version(void) { return CORUTV_VERSION; }
+
+int corutv_create(int device, void* stream, corutv_handle** out) {
+  if (!out) return CORUTV_ERR_ARG;
+  *out = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    cudaGetLastError();
+    return CORUTV_ERR_CUDA;
+  }
+  corutv_handle* h = new corutv_handle();
+  h->device = device;
+  h->stream = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaMallocHost(&h->pinned, 64 * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    delete h;
+    return CORUTV_ERR_NOMEM;
+  }
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
+  *out = h;
+  return CORUTV_OK;
+}
+
+void corutv_destroy(corutv_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  else cudaDeviceSynchronize();
+  if (h->arena) cudaFree(h->arena);
+  if (h->pinned) cudaFreeHost(h->pinned);
+  delete h;
+}
+
+int corutv_set_stream(corutv_handle* hh, void* stream) {
+  if (!hh) return CORUTV_ERR_ARG;
+  hh->stream = reinterpret_cast<cudaStream_t>(stream);
+  return CORUTV_OK;
+}
+
+const char* corutv_last_error(const corutv_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+int corutv_set_comm(corutv_handle* h, corutv_allreduce_fn fn, void* user, int rank, int world) {
+  if (!h || world < 1 || rank < 0 || rank >= world) return CORUTV_ERR_ARG;
+  h->ar_fn = fn;
+  h->ar_user = user;
+  h->rank = rank;
+  h->world = world;
+  return CORUTV_OK;
+}
+
+int corutv_decompose(corutv_handle* hh, const double* a, int64_t m, int64_t n, int64_t lda, int ell,
+                     int q_power, int variant, const double* omega, double* u, double* t, double* v,
+                     int64_t* perm, int64_t* passes_host) {
+  ABI_BEGIN(hh)
+  decompose(h, a, m, n, lda, ell, q_power, variant, omega, u, t, v, perm, passes_host);
+  ABI_END
+}
+
+int corutv_gemm(corutv_handle* hh, int trans_a, int64_t M, int64_t N, int64_t K, const double* a,
+                int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc) {
+  ABI_BEGIN(hh)
+  if (M < 0 || N < 0 || K < 0) fail(h, CORUTV_ERR_ARG, "negative dimension");
+  const int64_t ldbt = round_up(std::max<int64_t>(K, 1), 16);
+  // operands that TMA cannot address directly (odd ld / unaligned) are staged
+  const bool a_ok = ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && (lda % 2 == 0);
+  const bool b_ok = ((reinterpret_cast<uintptr_t>(b) & 15) == 0) && (ldb % 2 == 0);
+  const int64_t arows = trans_a ? K : M, acols = trans_a ? M : K;
+  const int64_t ldap = round_up(std::max<int64_t>(acols, 1), 16);
+  const int64_t ldbp = round_up(std::max<int64_t>(N, 1), 16);
+  Arena ar{h};
+  double *bt = nullptr, *ws = nullptr, *ap = nullptr, *bp = nullptr;
+  if (!trans_a) ar.add(&bt, (size_t)N * ldbt + 16);
+  if (!a_ok) ar.add(&ap, (size_t)arows * ldap + 16);
+  if (trans_a && !b_ok) ar.add(&bp, (size_t)K * ldbp + 16);
+  ar.add(&ws, gemm_ws_elems(h, M, N, K) + 16);
+  ar.commit();
+  if (!a_ok && arows > 0 && acols > 0) {
+    copy2d(h, a, arows, acols, lda, ap, ldap);
+    a = ap;
+    lda = ldap;
+  }
+  if (!trans_a) {
+    transpose(h, b, K, N, ldb, bt, ldbt);
+    run_gemm(h, false, M, N, K, a, lda, bt, ldbt, c, ldc, nullptr, 0, ws);
+  } else {
+    if (!b_ok && K > 0 && N > 0) {
+      copy2d(h, b, K, N, ldb, bp, ldbp);
+      b = bp;
+      ldb = ldbp;
+    }
+    run_gemm(h, true, M, N, K, a, lda, b, ldb, c, ldc, nullptr, 0, ws);
+  }
+  ABI_END
+}
+
+int corutv_alm_update(corutv_handle* hh, const double* m_mat, double* s, double* y, double* g_next,
+                      int64_t rows, int64_t cols, const double* u, const double* t, const double* v,
+                      int ell, int r, double mu, double lam_over_mu, double mu_next, double* zeta2_host,
+                      int64_t* nnz_host) {
+  ABI_BEGIN(hh)
+  gemm::LrParams p{};
+  p.ld = cols;
+  p.m_mat = m_mat;
+  p.s = s;
+  p.y = y;
+  p.g_next = g_next;
+  p.mu = mu;
+  p.lam_over_mu = lam_over_mu;
+  p.mu_next = mu_next;
+  double o[2] = {0, 0};
+  lowrank_op(h, gemm::LR_ALM, u, t, v, rows, cols, ell, r, p, o);
+  if (zeta2_host) *zeta2_host = o[0];
+  if (nnz_host) *nnz_host = (int64_t)llround(o[1]);
+  ABI_END
+}
+
+int corutv_lowrank(corutv_handle* hh, const double* u, const double* t, const double* v, int64_t rows,
+                   int64_t cols, int ell, int r, double* l_out) {
+  ABI_BEGIN(hh)
+  gemm::LrParams p{};
+  p.ld = cols;
+  p.g_next = l_out;
+  double o[2];
+  lowrank_op(h, gemm::LR_STORE, u, t, v, rows, cols, ell, r, p, o);
+  ABI_END
+}
+
+int corutv_lowrank_error(corutv_handle* hh, const double* a, int64_t m, int64_t n, int64_t lda,
+                         const double* u, const double* t, const double* v, int ell, double* out_host) {
+  ABI_BEGIN(hh)
+  gemm::LrParams p{};
+  p.ld = lda;
+  p.m_mat = a;
+  double o[2] = {0, 0};
+  lowrank_op(h, gemm::LR_RESID, u, t, v, m, n, ell, ell, p, o);
+  if (out_host) *out_host = std::sqrt(o[0]);
+  ABI_END
+}
+
+int corutv_spectral_norm(corutv_handle* hh, const double* a, int64_t m, int64_t n, int64_t lda, double tol,
+                         int max_iter, double* out_host, int* iters_host) {
+  ABI_BEGIN(hh)
+  double o = 0.0;
+  int it = 0;
+  spectral_norm(h, a, m, n, lda, tol, max_iter, &o, &it);
+  if (out_host) *out_host = o;
+  if (iters_host) *iters_host = it;
+  ABI_END
+}
+
+int corutv_singular_values(corutv_handle* hh, const double* a, int64_t m, int64_t n, int64_t lda,
+                           double* sig) {
+  ABI_BEGIN(hh)
+  singular_values(h, a, m, n, lda, sig);
+  ABI_END
+}
+
+int corutv_sumsq(corutv_handle* hh, const double* a, int64_t m, int64_t n, int64_t lda, double* out_host) {
+  ABI_BEGIN(hh)
+  const double v = sumsq(h, a, m, n, lda);
+  if (out_host) *out_host = v;
+  ABI_END
+}
+
+}  // extern "C"

@@ -1,0 +1,331 @@
+// FP64 tensor-core (DMMA) GEMMs for the CoR-UTV sketch contractions.
+//
+// Two operand orientations, both fed by TMA (cp.async.bulk.tensor, 128-byte
+// swizzle) through an mbarrier full/empty ring, one producer warp and eight
+// consumer warps issuing mma.sync.m8n8k4.f64 (SASS DMMA.884):
+//
+//   KK ("both K-major"):  C[M x N] = A[M x K] * Bt[N x K]^T
+//        A·Ω, A·Q2 (sketch.py:149,158), X·R^-1 (QR), Q1·Q~ (sketch.py:205),
+//        U_r·(T_r V')  (rpca.py:129) with fused ALM / residual epilogues.
+//   MM ("both M-major"):  C[M x N] = A[K x M]^T * B[K x N]
+//        A'·C1 (sketch.py:153), Gram X'X (QR), Q1'·(A Q2) (sketch.py:158).
+//
+// CTA tile: 128 rows x 16J columns (J = 1..8), warps 4 (M) x 2 (N), each warp
+// 32 x 8J.  One stage = 16 k-values: A tile 16 KB + B tile 2J KB.  For KK the
+// fragment lanes read k = 4s + (lane&3) (conflict-free on the swizzled
+// K-major rows); for MM they read rows k = s + 4*(lane&3) — a k permutation
+// (both operands use it, so the contraction is unchanged) that makes the
+// M-major swizzled tiles conflict-free as well.
+#pragma once
+#include "common.cuh"
+
+namespace gemm {
+
+constexpr int BM = 128;
+constexpr int BK = 16;
+constexpr int NCW = 8;                 // warps (all compute; thread 0 also issues TMA)
+constexpr int THREADS = NCW * 32;       // 2 warps per SMSP -> up to 255 registers each
+constexpr int SMEM_BUDGET = 200 * 1024;
+
+__host__ __device__ constexpr int a_stage_bytes() { return BM * BK * 8; }
+__host__ __device__ constexpr int b_stage_bytes(int J) { return 16 * J * BK * 8; }
+__host__ __device__ constexpr int stage_bytes(int J) { return a_stage_bytes() + b_stage_bytes(J); }
+__host__ __device__ constexpr int num_stages(int J) {
+  return (SMEM_BUDGET - 1024) / stage_bytes(J) > 8 ? 8 : (SMEM_BUDGET - 1024) / stage_bytes(J);
+}
+__host__ __device__ constexpr int smem_bytes(int J) {
+  return 1024 /*align slack*/ + num_stages(J) * stage_bytes(J) + 2 * 8 * 8 + 64;
+}
+
+struct Tile {
+  int M, N, K;          // problem (this launch)
+  int m_tiles, n_tiles;
+  int k_tiles;          // total k tiles (ceil(K / 16))
+  int k_tiles_per_split;
+  int splits;
+};
+
+// Accumulator for one consumer warp: 4 (M) x J (N) DMMA fragments.
+template <int J>
+struct Acc {
+  double v[4][J][2];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < J; ++j) v[i][j][0] = v[i][j][1] = 0.0;
+  }
+};
+
+struct Smem {
+  double* a;        // [stages][BM*BK]
+  double* b;        // [stages][16J*BK]
+  uint64_t* full;   // [stages]
+  uint64_t* empty;  // [stages]
+};
+
+template <int J>
+__device__ __forceinline__ Smem carve(unsigned char* raw) {
+  uintptr_t p = (reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023);
+  constexpr int S = num_stages(J);
+  Smem s;
+  s.a = reinterpret_cast<double*>(p);
+  s.b = reinterpret_cast<double*>(p + S * a_stage_bytes());
+  s.full = reinterpret_cast<uint64_t*>(p + S * (a_stage_bytes() + b_stage_bytes(J)));
+  s.empty = s.full + 8;
+  return s;
+}
+
+// Issue the TMA loads of k tile `kt` into ring slot `st` (thread 0 only).
+template <int J, bool MM>
+__device__ __forceinline__ void issue_stage(const Smem& sm, const CUtensorMap* mapA,
+                                            const CUtensorMap* mapB, int m0, int n0, int kt,
+                                            int st) {
+  mbar_arrive_expect_tx(&sm.full[st], stage_bytes(J));
+  double* sa = sm.a + st * (BM * BK);
+  double* sb = sm.b + st * (16 * J * BK);
+  if (!MM) {
+    tma_load_2d(sa, mapA, &sm.full[st], kt * BK, m0);
+    tma_load_2d(sb, mapB, &sm.full[st], kt * BK, n0);
+  } else {
+#pragma unroll
+    for (int bx = 0; bx < BM / 16; ++bx)
+      tma_load_2d(sa + bx * 16 * BK, mapA, &sm.full[st], m0 + 16 * bx, kt * BK);
+#pragma unroll
+    for (int bx = 0; bx < J; ++bx)
+      tma_load_2d(sb + bx * 16 * BK, mapB, &sm.full[st], n0 + 16 * bx, kt * BK);
+  }
+}
+
+// Pipelined mainloop over k tiles [kt0, kt1).  Thread 0 keeps S-1..S stages
+// in flight: at iteration i it refills the slot released at iteration i-1
+// (waiting on that slot's `empty` barrier, i.e. on the slowest warp), so the
+// wait almost never stalls.  Every warp: wait full -> 4 DMMA k-steps ->
+// arrive empty.  nvf / mvf: valid 8-col / 8-row fragments of this warp.
+template <int J, bool MM, bool CHECK>
+__device__ __forceinline__ void mainloop(const Smem& sm, const CUtensorMap* mapA,
+                                         const CUtensorMap* mapB, int m0, int n0, int kt0,
+                                         int kt1, Acc<J>& acc, int wm, int wn, int lane, int nvf,
+                                         int mvf, bool& bad) {
+  constexpr int S = num_stages(J);
+  const int nkt = kt1 - kt0;
+  const bool leader = threadIdx.x == 0;
+  if (leader) {
+    tma_prefetch_desc(mapA);
+    tma_prefetch_desc(mapB);
+    for (int i = 0; i < S && i < nkt; ++i) issue_stage<J, MM>(sm, mapA, mapB, m0, n0, kt0 + i, i);
+  }
+  const int r8 = lane >> 2, c4 = lane & 3;
+  for (int i = 0; i < nkt; ++i) {
+    const int st = i % S;
+    const uint32_t ph = (i / S) & 1;
+    if (leader && i >= 1 && (i - 1) + S < nkt) {
+      const int ps = (i - 1) % S;
+      mbar_wait(&sm.empty[ps], ((i - 1) / S) & 1);
+      issue_stage<J, MM>(sm, mapA, mapB, m0, n0, kt0 + (i - 1) + S, ps);
+    }
+    mbar_wait(&sm.full[st], ph);
+    const double* sa = sm.a + st * (BM * BK);
+    const double* sb = sm.b + st * (16 * J * BK);
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      double af[4], bf[J];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        const int row = wm * 32 + mi * 8 + r8;  // output row within tile
+        if (!MM) {
+          af[mi] = sa[swz128(row, s * 4 + c4)];
+        } else {
+          const int k = s + 4 * c4;
+          af[mi] = sa[(row >> 4) * (16 * BK) + swz128(k, row & 15)];
+        }
+        if (CHECK) bad |= is_nonfinite(af[mi]);
+      }
+#pragma unroll
+      for (int nj = 0; nj < J; ++nj) {
+        const int col = wn * 8 * J + nj * 8 + r8;
+        if (!MM) {
+          bf[nj] = sb[swz128(col, s * 4 + c4)];
+        } else {
+          const int k = s + 4 * c4;
+          bf[nj] = sb[(col >> 4) * (16 * BK) + swz128(k, col & 15)];
+        }
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        if (mi < mvf) {
+#pragma unroll
+          for (int nj = 0; nj < J; ++nj)
+            if (nj < nvf) dmma884(acc.v[mi][nj][0], acc.v[mi][nj][1], af[mi], bf[nj]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[st]);
+  }
+}
+
+template <int J>
+__device__ __forceinline__ void init_barriers(const Smem& sm) {
+  constexpr int S = num_stages(J);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.empty[i], NCW);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+}
+
+// -------------------------------------------------------------- plain GEMM
+struct StoreParams {
+  double* c;       // direct output (splits == 1) or partial workspace
+  int64_t ldc;
+  int64_t split_stride;  // elements between split partials (0 when direct)
+  int* bad_flag;         // nullable: set to 1 if a non-finite A entry was read
+};
+
+template <int J, bool MM, bool CHECK>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                Tile t, StoreParams sp) {
+  extern __shared__ unsigned char smem_raw[];
+  Smem sm = carve<J>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bid = blockIdx.x;
+  const int nt = bid % t.n_tiles;
+  const int rest = bid / t.n_tiles;
+  const int m0 = (rest % t.m_tiles) * BM;
+  const int split = rest / t.m_tiles;
+  const int n0 = nt * 16 * J;
+  const int kt0 = split * t.k_tiles_per_split;
+  const int kt1 = min(t.k_tiles, kt0 + t.k_tiles_per_split);
+  init_barriers<J>(sm);
+  const int wm = warp & 3, wn = warp >> 2;
+  const int ncol0 = n0 + wn * 8 * J;
+  const int nvf = max(0, min(J, (t.N - ncol0 + 7) / 8));
+  const int mvf = max(0, min(4, (t.M - (m0 + wm * 32) + 7) / 8));
+  Acc<J> acc;
+  acc.zero();
+  bool bad = false;
+  mainloop<J, MM, CHECK>(sm, &mapA, &mapB, m0, n0, kt0, kt1, acc, wm, wn, lane, nvf, mvf, bad);
+  if (CHECK && sp.bad_flag) {
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(sp.bad_flag, 1);
+  }
+  double* out = sp.c + (int64_t)split * sp.split_stride;
+  const int r8 = lane >> 2, c4 = lane & 3;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int row = m0 + wm * 32 + mi * 8 + r8;
+    if (row >= t.M) continue;
+#pragma unroll
+    for (int nj = 0; nj < J; ++nj) {
+      const int col = ncol0 + nj * 8 + 2 * c4;
+      double* p = out + (int64_t)row * sp.ldc + col;
+      if (col < t.N) p[0] = acc.v[mi][nj][0];
+      if (col + 1 < t.N) p[1] = acc.v[mi][nj][1];
+    }
+  }
+}
+
+// ------------------------------------------------ low-rank product epilogues
+// C = U_r * Wt^T (K = r) is never stored as a whole; the epilogue consumes
+// each 128 x 16J tile in registers.
+enum LrMode { LR_STORE = 0, LR_ALM = 1, LR_RESID = 2 };
+
+struct LrParams {
+  int64_t ld;            // leading dimension of all n x n operands
+  const double* m_mat;   // ALM: M ; RESID: A
+  double* s;             // ALM: S out
+  double* y;             // ALM: Y in/out
+  double* g_next;        // ALM: next G out ; STORE: L out
+  double mu, lam_over_mu, mu_next;
+  double* part_sum;      // per-CTA partial sum of squares
+  long long* part_cnt;   // per-CTA partial nnz
+};
+
+template <int J, int MODE>
+__global__ void __launch_bounds__(THREADS, 1)
+    lowrank_kernel(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapW,
+                   Tile t, LrParams p) {
+  extern __shared__ unsigned char smem_raw[];
+  __shared__ double red_sum[NCW];
+  __shared__ long long red_cnt[NCW];
+  Smem sm = carve<J>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bid = blockIdx.x;
+  const int nt = bid % t.n_tiles;
+  const int m0 = (bid / t.n_tiles) * BM;
+  const int n0 = nt * 16 * J;
+  init_barriers<J>(sm);
+  const int wm = warp & 3, wn = warp >> 2;
+  const int ncol0 = n0 + wn * 8 * J;
+  const int nvf = max(0, min(J, (t.N - ncol0 + 7) / 8));
+  const int mvf = max(0, min(4, (t.M - (m0 + wm * 32) + 7) / 8));
+  Acc<J> acc;
+  acc.zero();
+  bool bad = false;
+  mainloop<J, false, false>(sm, &mapU, &mapW, m0, n0, 0, t.k_tiles, acc, wm, wn, lane, nvf, mvf, bad);
+
+  const int r8 = lane >> 2, c4 = lane & 3;
+  double ssum = 0.0;
+  long long cnt = 0;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int row = m0 + wm * 32 + mi * 8 + r8;
+    if (row >= t.M) continue;
+#pragma unroll
+    for (int nj = 0; nj < J; ++nj) {
+      const int col = ncol0 + nj * 8 + 2 * c4;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (col + e >= t.N) continue;
+        const int64_t idx = (int64_t)row * p.ld + col + e;
+        const double l = acc.v[mi][nj][e];
+        if (MODE == LR_STORE) {
+          p.g_next[idx] = l;
+        } else if (MODE == LR_RESID) {
+          const double d = p.m_mat[idx] - l;
+          ssum = fma(d, d, ssum);
+        } else {
+          // rpca.py:211-214, operation order mirrored from the numpy source
+          const double mm = p.m_mat[idx];
+          const double yy = p.y[idx];
+          const double g = (mm - l) + yy / p.mu;
+          const double ag = fabs(g) - p.lam_over_mu;
+          const double sg = (g > 0.0) ? 1.0 : ((g < 0.0) ? -1.0 : g);
+          const double sv = sg * fmax(ag, 0.0);
+          const double z = (mm - l) - sv;
+          const double yn = yy + p.mu * z;
+          p.s[idx] = sv;
+          p.y[idx] = yn;
+          p.g_next[idx] = (mm - sv) + yn / p.mu_next;
+          ssum = fma(z, z, ssum);
+          cnt += (fabs(sv) > 1e-12) ? 1 : 0;
+        }
+      }
+    }
+  }
+  if (MODE != LR_STORE) {
+    ssum = warp_sum(ssum);
+    cnt = warp_sum(cnt);
+    if (lane == 0) {
+      red_sum[warp] = ssum;
+      red_cnt[warp] = cnt;
+    }
+    __syncthreads();
+    if (warp == 0 && lane == 0) {
+      double s2 = 0.0;
+      long long c2 = 0;
+      for (int w = 0; w < NCW; ++w) {
+        s2 += red_sum[w];
+        c2 += red_cnt[w];
+      }
+      p.part_sum[bid] = s2;
+      if (p.part_cnt) p.part_cnt[bid] = c2;
+    }
+  }
+}
+
+}  // namespace gemm

@@ -1,0 +1,65 @@
+"""Dense kernels used on the hot path, device-backed — the subset of
+/root/reference/pkg/src/corutv/dense.py that CoR-UTV and ALM-CoRUTV call.
+
+* :func:`spectral_norm` — dense.py:405-442 (mu0 of the ALM solver)
+* :func:`singular_values` — dense.py:379-387 (rank readout of L)
+* :func:`frobenius_norm` — dense.py:94-96
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+from . import _device as dev
+from . import _lib
+
+__all__ = ["spectral_norm", "singular_values", "frobenius_norm", "spectral_norm_iters"]
+
+
+def spectral_norm_iters(a, tol: float = 1e-10, max_iter: int = 5000):
+    """(|A|_2, power iterations) — dense.py:405-442 schedule on the device:
+    block size min(24, n), disjoint-support start, stop when
+    |est - prev| <= 0.02 tol est; Jacobi path for min(m, n) <= 64."""
+    A, _ = dev.to_device(a, "a")
+    out = ctypes.c_double(0.0)
+    it = ctypes.c_int(0)
+    h = _lib.handle(A.device.index)
+    try:
+        h.call("corutv_spectral_norm", dev.ptr(A), A.shape[0], A.shape[1], A.stride(0), tol,
+               max_iter, ctypes.byref(out), ctypes.byref(it))
+    except ValueError:
+        dev.raise_if_nonfinite(A, "a")
+        raise
+    if not math.isfinite(out.value):
+        dev.raise_if_nonfinite(A, "a")
+    return float(out.value), int(it.value)
+
+
+def spectral_norm(a, tol: float = 1e-10, max_iter: int = 5000) -> float:
+    """Largest singular value (dense.py:405-442)."""
+    return spectral_norm_iters(a, tol, max_iter)[0]
+
+
+def singular_values(a):
+    """Singular values, descending (dense.py:379-387), one-sided Jacobi on
+    the device.  Small matrices only (min(m, n) <= 640)."""
+    torch = dev.torch_mod()
+    A, was_host = dev.to_device(a, "a")
+    dev.raise_if_nonfinite(A, "a")
+    k = min(A.shape)
+    sig = torch.empty((k,), dtype=torch.float64, device=A.device)
+    h = _lib.handle(A.device.index)
+    h.call("corutv_singular_values", dev.ptr(A), A.shape[0], A.shape[1], A.stride(0), dev.ptr(sig))
+    return dev.to_output(sig, was_host)
+
+
+def frobenius_norm(a) -> float:
+    """dense.py:94-96 with a deterministic two-stage device reduction."""
+    A, _ = dev.to_device(a, "a")
+    out = ctypes.c_double(0.0)
+    h = _lib.handle(A.device.index)
+    h.call("corutv_sumsq", dev.ptr(A), A.shape[0], A.shape[1], A.stride(0), ctypes.byref(out))
+    if not math.isfinite(out.value):
+        dev.raise_if_nonfinite(A, "a")
+    return math.sqrt(out.value)

@@ -1,0 +1,123 @@
+"""Row-sharded (multi-GPU) CoR-UTV — SURVEY §8e.
+
+One process per GPU; rank g owns a contiguous block of rows A_g.  The
+native library does all the math and calls back into this module at the
+exchange points of the algorithm (sum-allreduce on the handle's stream):
+
+  * C2 = sum_g A_g' C1_g                 (n x ell, per power iteration)
+  * Gram X'X of the row-sharded Q1 sketch (ell x ell, per CholeskyQR step)
+  * D  = sum_g Q1_g' (A_g Q2)            (ell x ell)
+  * the global row count, the non-finite flag, ALM (zeta^2, nnz) scalars
+
+Everything replicated (Q2, the QRCP of D, V) is computed redundantly and
+bit-identically on every rank from the all-reduced inputs.  The callback is
+bound to ``torch.distributed.all_reduce`` (NCCL over NVLink on GPUs; gloo
+in the CPU tests).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _device as dev
+from . import _lib
+from .sketch import _VARIANT_CODE, CorUtvFactors, PassCounter, SketchConfig, gaussian_matrix
+
+__all__ = ["row_range", "RowShardComm", "corutv_sharded"]
+
+
+def row_range(m: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous block of rows owned by ``rank``: the first m % world ranks
+    get one extra row."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    base, extra = divmod(m, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+class _CudaBuffer:
+    """Zero-copy view of a raw device pointer for torch.as_tensor."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {
+            "shape": (count,), "typestr": "<f8", "data": (ptr, False), "version": 3,
+            "strides": None,
+        }
+
+
+class RowShardComm:
+    """Sum-allreduce callback for the native library over a torch.distributed
+    process group.  ``device``: "cuda" (pointers are device memory) or
+    "cpu" (host pointers; used by the gloo tests of the marshalling)."""
+
+    def __init__(self, group=None, device: str = "cuda"):
+        import torch.distributed as tdist
+
+        self.group = group
+        self.rank = tdist.get_rank(group)
+        self.world = tdist.get_world_size(group)
+        self.device = device
+        self.calls = 0
+        self.callback = _lib.ALLREDUCE_FN(self._allreduce)
+
+    def _tensor(self, ptr: int, count: int):
+        import torch
+
+        if self.device == "cpu":
+            arr = np.ctypeslib.as_array((ctypes.c_double * count).from_address(ptr))
+            return torch.from_numpy(arr)
+        return torch.as_tensor(_CudaBuffer(ptr, count), device="cuda")
+
+    def _allreduce(self, user, buf, count, stream):  # noqa: ARG002
+        import torch.distributed as tdist
+
+        try:
+            t = self._tensor(int(buf), int(count))
+            tdist.all_reduce(t, op=tdist.ReduceOp.SUM, group=self.group)
+            self.calls += 1
+            return 0
+        except Exception:  # pragma: no cover - surfaced as CORUTV_ERR_COMM
+            return 1
+
+    def attach(self, handle: "_lib.Handle") -> None:
+        _lib.check(handle.lib.corutv_set_comm(handle.ptr, self.callback, None, self.rank, self.world),
+                   handle.ptr, "corutv_set_comm")
+
+    def detach(self, handle: "_lib.Handle") -> None:
+        handle.lib.corutv_set_comm(handle.ptr, _lib.ALLREDUCE_FN(), None, 0, 1)
+
+
+def corutv_sharded(a_local, cfg: SketchConfig, comm: RowShardComm, counter: PassCounter | None = None,
+                   omega=None) -> CorUtvFactors:
+    """CoR-UTV of the row-sharded global matrix whose rows
+    ``row_range(m, world, rank)`` are ``a_local`` on this rank.  Returns the
+    local rows of U plus the replicated T and V."""
+    torch = dev.torch_mod()
+    A, was_host = dev.to_device(a_local, "a")
+    m_loc, n = A.shape
+    ell = cfg.ell
+    if omega is None:
+        omega = gaussian_matrix(n, ell, cfg.seed)  # identical on every rank
+    om = (omega if dev.is_device_tensor(omega) else torch.from_numpy(np.ascontiguousarray(omega)))
+    om = om.to(A.device, torch.float64).contiguous()
+    u = torch.empty((m_loc, ell), dtype=torch.float64, device=A.device)
+    t = torch.empty((ell, ell), dtype=torch.float64, device=A.device)
+    v = torch.empty((n, ell), dtype=torch.float64, device=A.device)
+    perm = torch.empty((ell,), dtype=torch.int64, device=A.device)
+    passes = ctypes.c_int64(0)
+    h = _lib.handle(A.device.index)
+    comm.attach(h)
+    try:
+        h.call("corutv_decompose", dev.ptr(A), m_loc, n, A.stride(0), ell, cfg.q_power,
+               _VARIANT_CODE[cfg.variant], dev.ptr(om), dev.ptr(u), dev.ptr(t), dev.ptr(v),
+               dev.ptr(perm), ctypes.byref(passes))
+    finally:
+        comm.detach(h)
+    if counter is not None:
+        counter.add(passes.value)
+    return CorUtvFactors(u=dev.to_output(u, was_host), t=dev.to_output(t, was_host),
+                         v=dev.to_output(v, was_host), ell=ell, q_power=cfg.q_power,
+                         variant=cfg.variant, perm=dev.to_output(perm, was_host))

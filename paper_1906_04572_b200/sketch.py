@@ -1,0 +1,213 @@
+"""CoR-UTV on the B200 — drop-in for the reference's ``corutv.sketch``.
+
+Same names, signatures, validation messages and result types as
+/root/reference/pkg/src/corutv/sketch.py; the numerics run in the sm_100a
+library (``corutv_decompose``, include/corutv_b200.h).
+
+Additive API: ``corutv(..., omega=None)`` accepts a
+caller-supplied n x ell Gaussian test matrix (default: ``gaussian_matrix(n,
+ell, seed)`` exactly as sketch.py:174), and :func:`corutv_kpq` takes the
+north-star's (A, k, p, q, omega) form with ell = k + p.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device as dev
+from . import _lib
+
+__all__ = [
+    "VARIANT_EXACT",
+    "VARIANT_APPROX",
+    "SketchConfig",
+    "CorUtvFactors",
+    "PassCounter",
+    "gaussian_matrix",
+    "corutv",
+    "corutv_kpq",
+    "corutv_lowrank_error",
+    "count_passes",
+    "flop_estimate",
+]
+
+VARIANT_EXACT = "exact-d"   # sketch.py:53
+VARIANT_APPROX = "approx-d"  # sketch.py:55
+_VARIANTS = (VARIANT_EXACT, VARIANT_APPROX)
+_VARIANT_CODE = {VARIANT_EXACT: _lib.EXACT_D, VARIANT_APPROX: _lib.APPROX_D}
+
+
+def gaussian_matrix(rows: int, cols: int, seed: int) -> np.ndarray:
+    """sketch.py:63-68: numpy PCG64(seed) ziggurat normals, host side.
+
+    The test matrix is an *input* of the decomposition; it is drawn with the
+    same numpy generator as the reference so that results are comparable on
+    identical seeds (SURVEY §7 "Omega parity")."""
+    if rows < 1 or cols < 1:
+        raise ValueError(f"gaussian_matrix needs positive dims, got {rows}x{cols}")
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return rng.standard_normal((rows, cols))
+
+
+@dataclass(frozen=True)
+class SketchConfig:
+    """sketch.py:71-98 — ell (sample size), q_power, seed, variant."""
+
+    ell: int
+    q_power: int = 0
+    seed: int = 0
+    variant: str = VARIANT_EXACT
+
+    def __post_init__(self):
+        if self.ell < 1:
+            raise ValueError(f"ell must be >= 1, got {self.ell}")
+        if self.q_power < 0:
+            raise ValueError(f"q_power must be >= 0, got {self.q_power}")
+        if self.variant not in _VARIANTS:
+            raise ValueError(f"variant must be one of {_VARIANTS}, got {self.variant!r}")
+
+    def validated_for(self, m: int, n: int) -> "SketchConfig":
+        if self.ell > min(m, n):
+            raise ValueError(
+                f"ell={self.ell} exceeds min(m, n)={min(m, n)} for a {m}x{n} input"
+            )
+        return self
+
+
+@dataclass
+class CorUtvFactors:
+    """sketch.py:101-123 — u (m x ell), t (ell x ell upper), v (n x ell).
+
+    Arrays are numpy for host inputs and torch CUDA tensors for device
+    inputs.  ``perm`` (extra) is the QRCP column permutation."""
+
+    u: object
+    t: object
+    v: object
+    ell: int
+    q_power: int
+    variant: str
+    perm: object = None
+
+    def lowrank(self):
+        """The rank-ell approximation u @ (t @ v.T) (sketch.py:117-119)."""
+        if dev.is_device_tensor(self.u):
+            from .rpca import _lowrank_device
+
+            return _lowrank_device(self.u, self.t, self.v, self.ell)
+        return self.u @ (self.t @ self.v.T)
+
+    def diag_abs(self):
+        """|diag(t)| (sketch.py:121-123)."""
+        if dev.is_device_tensor(self.t):
+            return self.t.diagonal().abs()
+        return np.abs(np.diag(self.t))
+
+
+@dataclass
+class PassCounter:
+    """sketch.py:126-133 — full sweeps over the data matrix."""
+
+    passes: int = 0
+
+    def add(self, n: int = 1) -> None:
+        self.passes += n
+
+
+def _omega_device(omega, n, ell, seed, device_like):
+    torch = dev.torch_mod()
+    if omega is None:
+        omega = gaussian_matrix(n, ell, seed)
+    if dev.is_device_tensor(omega):
+        om = omega.to(torch.float64).contiguous()
+    else:
+        om = torch.from_numpy(np.ascontiguousarray(omega, dtype=np.float64)).to(device_like.device)
+    if tuple(om.shape) != (n, ell):
+        raise ValueError(f"omega must be {n}x{ell}, got {tuple(om.shape)}")
+    return om
+
+
+def corutv(a, cfg: SketchConfig, counter: PassCounter | None = None, omega=None) -> CorUtvFactors:
+    """Compressed randomized UTV (sketch.py:182-208) on the B200.
+
+    Requires m >= n.  ``a``: numpy-compatible host array (copied to the
+    current CUDA device) or a CUDA tensor (used in place).  ``omega``:
+    optional caller-supplied n x ell test matrix."""
+    torch = dev.torch_mod()
+    a = dev.shape_check(a, "a")
+    m, n = (tuple(a.shape))
+    if m < n or cfg.ell > min(m, n):
+        # reference order: as_matrix's finiteness check comes first (dense.py:48)
+        t, _ = dev.to_device(a, "a")
+        dev.raise_if_nonfinite(t, "a")
+        if m < n:
+            raise ValueError(f"corutv requires rows >= cols, got {m}x{n}")
+        cfg.validated_for(m, n)
+    A, was_host = dev.to_device(a, "a")
+    ell = cfg.ell
+    om = _omega_device(omega, n, ell, cfg.seed, A)
+    u = torch.empty((m, ell), dtype=torch.float64, device=A.device)
+    t = torch.empty((ell, ell), dtype=torch.float64, device=A.device)
+    v = torch.empty((n, ell), dtype=torch.float64, device=A.device)
+    perm = torch.empty((ell,), dtype=torch.int64, device=A.device)
+    passes = ctypes.c_int64(0)
+    h = _lib.handle(A.device.index)
+    h.call("corutv_decompose", dev.ptr(A), m, n, A.stride(0), ell, cfg.q_power,
+           _VARIANT_CODE[cfg.variant], dev.ptr(om), dev.ptr(u), dev.ptr(t), dev.ptr(v),
+           dev.ptr(perm), ctypes.byref(passes))
+    if counter is not None:
+        counter.add(passes.value)
+    return CorUtvFactors(u=dev.to_output(u, was_host), t=dev.to_output(t, was_host),
+                         v=dev.to_output(v, was_host), ell=ell, q_power=cfg.q_power,
+                         variant=cfg.variant, perm=dev.to_output(perm, was_host))
+
+
+def corutv_kpq(a, k: int, p: int, q: int, omega=None, seed: int = 0,
+               variant: str = VARIANT_EXACT) -> CorUtvFactors:
+    """North-star form: target rank k, oversampling p (ell = k + p), q power
+    iterations, optional caller-supplied Gaussian test matrix."""
+    return corutv(a, SketchConfig(ell=k + p, q_power=q, seed=seed, variant=variant), omega=omega)
+
+
+def corutv_lowrank_error(a, cfg: SketchConfig, counter: PassCounter | None = None) -> float:
+    """sketch.py:211-217: |A - U T V'|_F, evaluated on the device without
+    materialising U T V' (one fused GEMM + residual pass)."""
+    torch = dev.torch_mod()
+    A, _ = dev.to_device(a, "a")
+    f = corutv(A, cfg, counter)
+    out = ctypes.c_double(0.0)
+    h = _lib.handle(A.device.index)
+    h.call("corutv_lowrank_error", dev.ptr(A), A.shape[0], A.shape[1], A.stride(0),
+           dev.ptr(f.u), dev.ptr(f.t), dev.ptr(f.v), f.ell, ctypes.byref(out))
+    del torch
+    return float(out.value)
+
+
+def count_passes(fn, a, cfg: SketchConfig) -> int:
+    """sketch.py:265-269."""
+    counter = PassCounter()
+    fn(a, cfg, counter)
+    return counter.passes
+
+
+def flop_estimate(m: int, n: int, ell: int, q_power: int = 0, variant: str = VARIANT_EXACT) -> int:
+    """sketch.py:272-296 — the algorithmic flop count (metric numerator)."""
+    if min(m, n, ell) < 1:
+        raise ValueError("dimensions must be positive")
+    if variant not in _VARIANTS:
+        raise ValueError(f"variant must be one of {_VARIANTS}, got {variant!r}")
+    reps = q_power + 1
+    total = n * ell
+    total += reps * 2 * m * n * ell
+    total += reps * 2 * m * n * ell
+    total += 2 * m * ell ** 2 + 2 * n * ell ** 2
+    if variant == VARIANT_EXACT:
+        total += m * ell ** 2 + 2 * m * n * ell
+    else:
+        total += 2 * m * ell ** 2 + 2 * n * ell ** 2 + 3 * ell ** 3
+    total += (8 * ell ** 3) // 3
+    total += 2 * m * ell ** 2 + 2 * n * ell
+    return total
