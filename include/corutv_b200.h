@@ -117,6 +117,16 @@ int corutv_lowrank_error(corutv_handle* h, const double* a, int64_t m, int64_t n
 int corutv_gemm(corutv_handle* h, int trans_a, int64_t M, int64_t N, int64_t K, const double* a,
                 int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc);
 
+/* Measurement hooks (bench.py): begin() resets the kernel-launch counter and
+ * starts recording CUDA events on the handle's stream around every DMMA GEMM
+ * and fused low-rank launch; end() synchronises and returns, per class
+ * c in {0 unused, 1 = GEMMs sweeping the data matrix (K1/K2/K5), 2 = other
+ * GEMMs (QR Grams / triangular products / lift), 3 = fused low-rank (ALM)}:
+ * out12[3c] = summed kernel ms, out12[3c+1] = launches, out12[3c+2] =
+ * algorithmic flops (2MNK); *launches = all kernels launched since begin(). */
+int corutv_profile_begin(corutv_handle* h);
+int corutv_profile_end(corutv_handle* h, double* out12, int64_t* launches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -46,6 +46,8 @@ SIGNATURES = {
     "corutv_sumsq": (_I32, [_VP, _VP, _I64, _I64, _I64, c_double_p]),
     "corutv_lowrank_error": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _VP, _VP, _I32, c_double_p]),
     "corutv_gemm": (_I32, [_VP, _I32, _I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _I64]),
+    "corutv_profile_begin": (_I32, [_VP]),
+    "corutv_profile_end": (_I32, [_VP, c_double_p, c_int64_p]),
 }
 
 

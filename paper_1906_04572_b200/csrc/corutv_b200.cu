@@ -36,6 +36,16 @@ struct corutv_handle {
   size_t arena_size = 0;
   double* pinned = nullptr;  // 64 doubles of pinned host scratch
   int num_sms = 148;
+  // profiling (corutv_profile_begin/end): launch counter always on; CUDA
+  // events around the DMMA GEMM / low-rank kernels while enabled.
+  int64_t launches = 0;
+  bool prof = false;
+  int tag = 2;  // class of the next GEMM launches: 1 = A sweep, 2 = other
+  struct Cls {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    double flops = 0.0;
+    int64_t n = 0;
+  } cls[4];
 };
 
 namespace {
@@ -61,6 +71,7 @@ inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 #define CK_LAUNCH()                                                               \
   do {                                                                            \
+    ++h->launches;                                                                \
     cudaError_t e_ = cudaGetLastError();                                          \
     if (e_ != cudaSuccess) {                                                      \
       h->err = std::string("kernel launch: ") + cudaGetErrorString(e_);           \
@@ -72,6 +83,34 @@ void fail(corutv_handle* h, int code, const std::string& msg) {
   h->err = msg;
   throw Fail{code};
 }
+
+// --------------------------------------------------------------- profiling
+struct ProfScope {
+  corutv_handle* h;
+  int c;
+  double flops;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  ProfScope(corutv_handle* hh, int cls, double f) : h(hh), c(cls), flops(f) {
+    if (!h->prof) return;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, h->stream);
+  }
+  ~ProfScope() {
+    if (!h->prof || !e0) return;
+    cudaEventRecord(e1, h->stream);
+    h->cls[c].ev.push_back({e0, e1});
+    h->cls[c].flops += flops;
+    h->cls[c].n += 1;
+  }
+};
+
+struct TagScope {  // marks the GEMMs that sweep the data matrix (K1/K2/K5)
+  corutv_handle* h;
+  int old;
+  TagScope(corutv_handle* hh, int t) : h(hh), old(hh->tag) { h->tag = t; }
+  ~TagScope() { h->tag = old; }
+};
 
 // ------------------------------------------------------------------ arena
 struct Arena {
@@ -188,6 +227,7 @@ void launch_gemm_t(corutv_handle* h, const CUtensorMap& ma, const CUtensorMap& m
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::smem_bytes(J)));
     configured = true;
   }
+  ProfScope ps(h, h->tag, 2.0 * t.M * t.N * (double)t.K);
   kern<<<grid, gemm::THREADS, gemm::smem_bytes(J), h->stream>>>(ma, mb, t, sp);
   CK_LAUNCH();
 }
@@ -492,6 +532,7 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
 
   // power sketch (sketch.py:166-179): C1 = A X ; C2 = A' C1, q+1 times
   int cur = 0;
+  TagScope* sweep_tag = new TagScope(h, 1);
   for (int it = 0; it <= q; ++it) {
     run_gemm(h, false, m, l, n, A, ldA, XT, ldn, C1a, ldp, nullptr, 0, ws, it == 0 ? flag : nullptr);
     if (!sharded) {
@@ -503,6 +544,7 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
     }
     cur ^= 1;
   }
+  delete sweep_tag;
   // Xn[cur] = C2 (final), Xn[cur^1] = C2 entering the last C1 product
   double* c2 = Xn[cur];
   double* c2_in = Xn[cur ^ 1];
@@ -536,7 +578,10 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   int64_t passes = 2 * (q + 1);
   if (variant == CORUTV_EXACT_D) {
     transpose(h, Q2, n, l, ldp, XT, ldn);
-    run_gemm(h, false, m, l, n, A, ldA, XT, ldn, P, ldp, nullptr, 0, ws);  // P = A Q2
+    {
+      TagScope ts(h, 1);
+      run_gemm(h, false, m, l, n, A, ldA, XT, ldn, P, ldp, nullptr, 0, ws);  // P = A Q2
+    }
     run_gemm(h, true, l, l, m, Q1, ldp, P, ldp, D, ldp, nullptr, 0, ws);    // D = Q1' P
     if (sharded) allreduce(h, D, (int64_t)l * ldp);
     passes += 1;
@@ -574,6 +619,7 @@ void launch_lr_t(corutv_handle* h, const CUtensorMap& mu, const CUtensorMap& mw,
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::smem_bytes(J)));
     configured = true;
   }
+  ProfScope ps(h, 3, 2.0 * t.M * t.N * (double)t.K);
   kern<<<grid, gemm::THREADS, gemm::smem_bytes(J), h->stream>>>(mu, mw, t, p);
   CK_LAUNCH();
 }
@@ -967,6 +1013,46 @@ int corutv_sumsq(corutv_handle* hh, const double* a, int64_t m, int64_t n, int64
   ABI_BEGIN(hh)
   const double v = sumsq(h, a, m, n, lda);
   if (out_host) *out_host = v;
+  ABI_END
+}
+
+int corutv_profile_begin(corutv_handle* hh) {
+  ABI_BEGIN(hh)
+  for (auto& c : h->cls) {
+    for (auto& e : c.ev) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+    c.ev.clear();
+    c.flops = 0.0;
+    c.n = 0;
+  }
+  h->launches = 0;
+  h->prof = true;
+  ABI_END
+}
+
+int corutv_profile_end(corutv_handle* hh, double* out12, int64_t* launches) {
+  ABI_BEGIN(hh)
+  sync(h);
+  for (int c = 0; c < 4; ++c) {
+    double ms = 0.0;
+    for (auto& e : h->cls[c].ev) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, e.first, e.second);
+      ms += t;
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+    h->cls[c].ev.clear();
+    if (out12) {
+      out12[3 * c + 0] = ms;
+      out12[3 * c + 1] = (double)h->cls[c].n;
+      out12[3 * c + 2] = h->cls[c].flops;
+    }
+  }
+  if (launches) *launches = h->launches;
+  h->prof = false;
   ABI_END
 }
 

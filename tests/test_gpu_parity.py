@@ -85,7 +85,12 @@ def test_corutv_matches_reference_golden(golden, name):
     check_factors(f, a, ell)
     na = np.linalg.norm(a)
     err = np.linalg.norm(a - f.lowrank())
-    assert abs(err - float(c["err"])) <= 1e-10 * na
+    if name == "cu_full_ell":
+        # ell == n: exact in exact arithmetic; both errors are round-off of a
+        # kappa(A)^3-conditioned sketch (reference: 2.2e-9 |A|)
+        assert err <= 1e-8 * na and float(c["err"]) <= 1e-8 * na
+    else:
+        assert abs(err - float(c["err"])) <= 1e-10 * na
     k = LEAD[name]
     dref = np.abs(np.diag(c["t"]))
     assert np.abs(np.abs(np.diag(f.t))[:k] - dref[:k]).max() <= 1e-9 * dref[0]
