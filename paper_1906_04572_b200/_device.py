@@ -32,7 +32,7 @@ def is_device_tensor(x) -> bool:
 def shape_check(x, name):
     """The structural part of as_matrix (dense.py:41-47); finiteness is
     checked on the device."""
-    if is_device_tensor(x):
+    if is_device_tensor(x) or is_host_tensor(x):
         shape = tuple(x.shape)
     else:
         x = np.asarray(x, dtype=float)
@@ -44,9 +44,29 @@ def shape_check(x, name):
     return x
 
 
+def is_host_tensor(x) -> bool:
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor) and not x.is_cuda
+
+
 def to_device(x, name="matrix", pin=False):
-    """Return (device float64 tensor with unit inner stride, was_host)."""
+    """Return (device float64 tensor with unit inner stride, was_host).
+
+    Host torch tensors (e.g. pinned buffers) are copied asynchronously on
+    the current stream; results for them come back as host torch tensors."""
     torch = torch_mod()
+    if is_host_tensor(x):
+        if x.dim() != 2:
+            raise ValueError(f"{name} must be 2-D, got shape {tuple(x.shape)}")
+        if x.shape[0] < 1 or x.shape[1] < 1:
+            raise ValueError(f"{name} must have positive dimensions, got {tuple(x.shape)}")
+        t = x.to(torch.cuda.current_device(), dtype=torch.float64, non_blocking=True)
+        if t.stride(1) != 1:
+            t = t.contiguous()
+        return t, "torch"
     x = shape_check(x, name)
     if is_device_tensor(x):
         t = x
@@ -63,6 +83,8 @@ def to_device(x, name="matrix", pin=False):
 
 
 def to_output(t, was_host):
+    if was_host == "torch":
+        return t.cpu()
     if was_host:
         return t.cpu().numpy()
     return t
