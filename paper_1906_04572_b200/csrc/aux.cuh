@@ -149,6 +149,10 @@ __global__ void fill2d_kernel(double* p, int64_t rows, int64_t cols, int64_t ld,
     p[(idx / cols) * ld + idx % cols] = v;
 }
 
+__global__ void flag_to_double_kernel(const int* f, double* d) {
+  if (threadIdx.x == 0) d[0] = (double)f[0];
+}
+
 __global__ void fill_kernel(double* p, int64_t n, double v) {
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
        idx += (int64_t)gridDim.x * blockDim.x)

@@ -64,7 +64,7 @@ CU_DEV void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, i
 // D(8x8) += A(8x4, row) * B(4x8, col).  Lane l holds A[l>>2][l&3],
 // B[l&3][l>>2], and C[l>>2][2*(l&3) + {0,1}].  SASS: DMMA.884.
 CU_DEV void dmma884(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }

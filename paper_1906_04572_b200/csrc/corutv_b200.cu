@@ -376,52 +376,89 @@ void set_smem(corutv_handle* h, K kern, size_t bytes) {
 }
 
 // ------------------------------------------------ adaptive CholeskyQR
-// In place of householder_qr(...).q (dense.py:132-149): returns the buffer
-// (xa or xb) that holds Q.  X has `rows` local rows (ld ldx), ell columns.
+// In place of householder_qr(...).q (dense.py:132-149).  Each step: Gram
+// G = X'X (DMMA, split-K; all-reduced when X is row-sharded), one-CTA
+// factor R = chol(G) [+ shift s = 11 (m l + l(l+1)) u tr(G) when the plain
+// factor fails or kappa_F(R) > 1e6], X <- X R^-1 (DMMA).  Two consecutive
+// unshifted steps (CholeskyQR2) end the iteration.  Several independent
+// matrices advance together so their host decisions share one sync.
 struct QrWork {
   double* G;      // ell x ldx
   double* rinvT;  // ell x ldx
   double* gwork;  // ell * ell
-  double* ws;     // split-K scratch
+  double* ws;     // split-K scratch (shared: stream-ordered)
   small::CholInfo* info;  // device
 };
 
-double* cholqr(corutv_handle* h, double* xa, double* xb, int64_t rows, int ell, int64_t ldx,
-               double rows_global, bool sharded, const QrWork& w, int* steps_out = nullptr) {
+struct QrJob {
+  double* cur;
+  double* nxt;
+  int64_t rows;
+  double rows_global;
+  bool sharded;
+  QrWork w;
+  int plain = 0;
+  bool done = false;
+  int steps = 0;
+};
+
+// extra_flag: optional device int read back with the first step's sync;
+// a nonzero value aborts with CORUTV_ERR_NONFINITE before any QR decision.
+void cholqr_multi(corutv_handle* h, QrJob* jobs, int njobs, int ell, int64_t ldx,
+                  const double* extra_flag = nullptr) {
   const int l = ell;
-  const double coeff = 11.0 * (rows_global * l + (double)l * (l + 1)) * kUnit;
   const size_t wbytes = (size_t)l * l * 8;
   const int optin = max_optin_smem(h);
   const bool smem = wbytes + 8 * 1024 <= (size_t)optin - 8 * 1024;
   if (smem) set_smem(h, small::chol_factor_kernel, wbytes);
-  double* cur = xa;
-  double* nxt = xb;
-  int plain = 0;
   for (int step = 0; step < kMaxQrSteps; ++step) {
-    run_gemm(h, true, l, l, rows, cur, ldx, cur, ldx, w.G, ldx, nullptr, 0, w.ws);
-    if (sharded) allreduce(h, w.G, (int64_t)l * ldx);
-    small::chol_factor_kernel<<<1, small::THREADS, smem ? wbytes : 0, h->stream>>>(
-        w.G, l, ldx, coeff, 1, kKappaPlain, w.rinvT, ldx, w.gwork, smem ? 1 : 0, w.info);
-    CK_LAUNCH();
-    run_gemm(h, false, rows, l, l, cur, ldx, w.rinvT, ldx, nxt, ldx, nullptr, 0, w.ws);
-    std::swap(cur, nxt);
-    CK(cudaMemcpyAsync(h->pinned, w.info, sizeof(small::CholInfo), cudaMemcpyDeviceToHost, h->stream));
-    sync(h);
-    small::CholInfo info;
-    std::memcpy(&info, h->pinned, sizeof(info));
-    if (info.status == 2) fail(h, CORUTV_ERR_NONFINITE, "sketch contains non-finite entries");
-    if (info.status == 1) {
-      if (steps_out) *steps_out = step + 1;
-      return cur;
+    int active = 0;
+    for (int j = 0; j < njobs; ++j) {
+      QrJob& q = jobs[j];
+      if (q.done) continue;
+      ++active;
+      const double coeff = 11.0 * (q.rows_global * l + (double)l * (l + 1)) * kUnit;
+      run_gemm(h, true, l, l, q.rows, q.cur, ldx, q.cur, ldx, q.w.G, ldx, nullptr, 0, q.w.ws);
+      if (q.sharded) allreduce(h, q.w.G, (int64_t)l * ldx);
+      small::chol_factor_kernel<<<1, small::THREADS, smem ? wbytes : 0, h->stream>>>(
+          q.w.G, l, ldx, coeff, 1, kKappaPlain, q.w.rinvT, ldx, q.w.gwork, smem ? 1 : 0, q.w.info);
+      CK_LAUNCH();
+      run_gemm(h, false, q.rows, l, l, q.cur, ldx, q.w.rinvT, ldx, q.nxt, ldx, nullptr, 0, q.w.ws);
+      std::swap(q.cur, q.nxt);
+      CK(cudaMemcpyAsync(h->pinned + 4 * j, q.w.info, sizeof(small::CholInfo), cudaMemcpyDeviceToHost,
+                         h->stream));
     }
-    plain = info.shifted ? 0 : plain + 1;
-    if (plain == 2) {
-      if (steps_out) *steps_out = step + 1;
-      return cur;
+    if (!active) return;
+    if (step == 0 && extra_flag)
+      CK(cudaMemcpyAsync(h->pinned + 60, extra_flag, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    sync(h);
+    if (step == 0 && extra_flag && h->pinned[60] != 0.0)
+      fail(h, CORUTV_ERR_NONFINITE, "a contains non-finite entries");
+    for (int j = 0; j < njobs; ++j) {
+      QrJob& q = jobs[j];
+      if (q.done) continue;
+      small::CholInfo info;
+      std::memcpy(&info, h->pinned + 4 * j, sizeof(info));
+      q.steps = step + 1;
+      if (info.status == 2) fail(h, CORUTV_ERR_NONFINITE, "sketch contains non-finite entries");
+      q.plain = info.shifted ? 0 : q.plain + 1;
+      if (info.status == 1 || q.plain == 2) q.done = true;
     }
   }
   fail(h, CORUTV_ERR_CONVERGENCE, "CholeskyQR did not reach orthogonality");
-  return nullptr;
+}
+
+double* cholqr(corutv_handle* h, double* xa, double* xb, int64_t rows, int ell, int64_t ldx,
+               double rows_global, bool sharded, const QrWork& w) {
+  QrJob j;
+  j.cur = xa;
+  j.nxt = xb;
+  j.rows = rows;
+  j.rows_global = rows_global;
+  j.sharded = sharded;
+  j.w = w;
+  cholqr_multi(h, &j, 1, ell, ldx);
+  return j.cur;
 }
 
 // --------------------------------------------------------------- QRCP
@@ -486,8 +523,8 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   const int64_t ldA = a_ok ? lda : round_up(n, 16);
 
   Arena ar{h};
-  double *Apad = nullptr, *Xn[2], *XT, *C1a, *C1b, *C2a, *C2b, *P, *G, *rinvT, *D, *qtT, *B1, *B2t, *pinvB;
-  double *gwork, *ws, *sigs;
+  double *Apad = nullptr, *Xn[2], *XT, *C1a, *C1b, *C2a, *P, *G, *rinvT, *D, *qtT, *B1, *B2t, *pinvB;
+  double *G2, *rinvT2, *gwork2, *gwork, *ws, *sigs, *flagd;
   int *flag, *perm32, *jstat;
   small::CholInfo* info;
   if (!a_ok) ar.add(&Apad, (size_t)m * ldA);
@@ -497,10 +534,13 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   ar.add(&C1a, (size_t)m * ldp);
   ar.add(&C1b, (size_t)m * ldp);
   ar.add(&C2a, (size_t)n * ldp);
-  ar.add(&C2b, (size_t)n * ldp);
   ar.add(&P, (size_t)m * ldp);
   ar.add(&G, (size_t)ldp * ldp);
   ar.add(&rinvT, (size_t)ldp * ldp);
+  ar.add(&G2, (size_t)ldp * ldp);
+  ar.add(&rinvT2, (size_t)ldp * ldp);
+  ar.add(&gwork2, 2 * (size_t)l * l + 16);
+  ar.add(&flagd, 2);
   ar.add(&D, (size_t)ldp * ldp);
   ar.add(&qtT, (size_t)ldp * ldp);
   ar.add(&B1, (size_t)ldp * ldp);
@@ -517,7 +557,7 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   ar.add(&flag, 4);
   ar.add(&perm32, (size_t)ldp);
   ar.add(&jstat, 4);
-  ar.add(&info, 2);
+  ar.add(&info, 4);
   ar.commit();
 
   const double* A = a;
@@ -548,31 +588,31 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   // Xn[cur] = C2 (final), Xn[cur^1] = C2 entering the last C1 product
   double* c2 = Xn[cur];
   double* c2_in = Xn[cur ^ 1];
-  if (sharded) {
-    // the non-finite flag must be agreed by all ranks before anything else
-    double* fd = gwork;  // reuse scratch: flag as double
-    CK(cudaMemcpyAsync(h->pinned, flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-    sync(h);
-    int fl = *reinterpret_cast<int*>(h->pinned);
-    h->pinned[1] = (double)fl;
-    CK(cudaMemcpyAsync(fd, h->pinned + 1, sizeof(double), cudaMemcpyHostToDevice, h->stream));
-    allreduce(h, fd, 1);
-    CK(cudaMemcpyAsync(h->pinned + 1, fd, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-    sync(h);
-    if (h->pinned[1] > 0.0) fail(h, CORUTV_ERR_NONFINITE, "a contains non-finite entries");
-  } else {
-    CK(cudaMemcpyAsync(h->pinned, flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-    sync(h);
-    if (*reinterpret_cast<int*>(h->pinned)) fail(h, CORUTV_ERR_NONFINITE, "a contains non-finite entries");
-  }
+  // non-finite flag (fused into the first A sweep) -> double, agreed by all
+  // ranks; read back together with the first QR decisions (no extra sync)
+  aux::flag_to_double_kernel<<<1, 32, 0, h->stream>>>(flag, flagd);
+  CK_LAUNCH();
+  if (sharded) allreduce(h, flagd, 1);
 
-  // orthonormalise both sketches (sketch.py:198-199)
-  QrWork w{G, rinvT, gwork, ws, info};
-  CK(cudaMemcpyAsync(C2a, c2, (size_t)n * ldp * 8, cudaMemcpyDeviceToDevice, h->stream));
+  // orthonormalise both sketches (sketch.py:198-199), advancing together
   if (variant == CORUTV_APPROX_D)
     CK(cudaMemcpyAsync(P, C1a, (size_t)m * ldp * 8, cudaMemcpyDeviceToDevice, h->stream));
-  double* Q1 = cholqr(h, C1a, C1b, m, l, ldp, mg, sharded, w);
-  double* Q2 = cholqr(h, C2a, C2b, n, l, ldp, (double)n, false, w);
+  QrJob jobs[2];
+  jobs[0].cur = C1a;
+  jobs[0].nxt = C1b;
+  jobs[0].rows = m;
+  jobs[0].rows_global = mg;
+  jobs[0].sharded = sharded;
+  jobs[0].w = QrWork{G, rinvT, gwork, ws, info};
+  jobs[1].cur = c2;
+  jobs[1].nxt = C2a;
+  jobs[1].rows = n;
+  jobs[1].rows_global = (double)n;
+  jobs[1].sharded = false;
+  jobs[1].w = QrWork{G2, rinvT2, gwork2, ws, info + 2};
+  cholqr_multi(h, jobs, 2, l, ldp, flagd);
+  double* Q1 = jobs[0].cur;
+  double* Q2 = jobs[1].cur;
 
   // compressed core (sketch.py:200-203)
   int64_t passes = 2 * (q + 1);

@@ -64,9 +64,12 @@ struct Smem {
   uint64_t* empty;  // [stages]
 };
 
+// Pointer arithmetic on the __shared__ array (never through an integer) so
+// the compiler keeps the shared address space and emits LDS.
 template <int J>
 __device__ __forceinline__ Smem carve(unsigned char* raw) {
-  uintptr_t p = (reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023);
+  const uint32_t pad = (1024u - (smem_u32(raw) & 1023u)) & 1023u;
+  unsigned char* p = raw + pad;
   constexpr int S = num_stages(J);
   Smem s;
   s.a = reinterpret_cast<double*>(p);
@@ -101,13 +104,25 @@ __device__ __forceinline__ void issue_stage(const Smem& sm, const CUtensorMap* m
 // in flight: at iteration i it refills the slot released at iteration i-1
 // (waiting on that slot's `empty` barrier, i.e. on the slowest warp), so the
 // wait almost never stalls.  Every warp: wait full -> 4 DMMA k-steps ->
-// arrive empty.  nvf / mvf: valid 8-col / 8-row fragments of this warp.
+// arrive empty.  All fragments are computed unconditionally (TMA zero-fills
+// out-of-range rows/columns), so the DMMA stream has no predicates.
+//
+// KK: both operands K-major, 128-B rows, 128-B swizzle.  A lane reads the
+//     16-byte chunk holding k = 8p + 2(lane&3) + {0,1}: one LDS.128 feeds
+//     k-steps 2p and 2p+1 (the k order inside a stage is permuted
+//     identically for A and B).  Physical chunk = (4p + (lane&3)) ^ (row&7):
+//     4 wavefronts per 512 B, the minimum.
+// MM: both operands M-major (16-column boxes, rows = k); lanes read rows
+//     k = s + 4(lane&3): the 4 rows of a fragment fall on two different
+//     (k & 7) swizzle phases, 2 wavefronts per 256 B, the minimum.
 template <int J, bool MM, bool CHECK>
 __device__ __forceinline__ void mainloop(const Smem& sm, const CUtensorMap* mapA,
                                          const CUtensorMap* mapB, int m0, int n0, int kt0,
                                          int kt1, Acc<J>& acc, int wm, int wn, int lane, int nvf,
                                          int mvf, bool& bad) {
   constexpr int S = num_stages(J);
+  (void)nvf;
+  (void)mvf;
   const int nkt = kt1 - kt0;
   const bool leader = threadIdx.x == 0;
   if (leader) {
@@ -116,6 +131,30 @@ __device__ __forceinline__ void mainloop(const Smem& sm, const CUtensorMap* mapA
     for (int i = 0; i < S && i < nkt; ++i) issue_stage<J, MM>(sm, mapA, mapB, m0, n0, kt0 + i, i);
   }
   const int r8 = lane >> 2, c4 = lane & 3;
+  // per-lane element offsets (in doubles) inside one stage
+  int offA[2], offB[2];      // KK: chunk offsets for the two k pairs
+  int rowA = 0, rowB = 0;    // KK: row bases
+  int mmA[4][4], mmB[4];     // MM: per (s, mi) A offsets; per s B base offsets
+  if (!MM) {
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      offA[p] = ((4 * p + c4) ^ r8) << 1;
+      offB[p] = offA[p];
+    }
+    rowA = (wm * 32 + r8) * 16;
+    rowB = (wn * 8 * J + r8) * 16;
+  } else {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int k = s + 4 * c4;
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        const int row = wm * 32 + mi * 8 + r8;
+        mmA[s][mi] = (row >> 4) * (16 * BK) + swz128(k, row & 15);
+      }
+      mmB[s] = k * 16;
+    }
+  }
   for (int i = 0; i < nkt; ++i) {
     const int st = i % S;
     const uint32_t ph = (i / S) & 1;
@@ -127,37 +166,45 @@ __device__ __forceinline__ void mainloop(const Smem& sm, const CUtensorMap* mapA
     mbar_wait(&sm.full[st], ph);
     const double* sa = sm.a + st * (BM * BK);
     const double* sb = sm.b + st * (16 * J * BK);
+    if (!MM) {
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      double af[4], bf[J];
+      for (int p = 0; p < 2; ++p) {
+        double2 a2[4], b2[J];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) {
-        const int row = wm * 32 + mi * 8 + r8;  // output row within tile
-        if (!MM) {
-          af[mi] = sa[swz128(row, s * 4 + c4)];
-        } else {
-          const int k = s + 4 * c4;
-          af[mi] = sa[(row >> 4) * (16 * BK) + swz128(k, row & 15)];
+        for (int mi = 0; mi < 4; ++mi) {
+          a2[mi] = *reinterpret_cast<const double2*>(sa + rowA + mi * 8 * 16 + offA[p]);
+          if (CHECK) bad |= is_nonfinite(a2[mi].x) | is_nonfinite(a2[mi].y);
         }
-        if (CHECK) bad |= is_nonfinite(af[mi]);
+#pragma unroll
+        for (int nj = 0; nj < J; ++nj)
+          b2[nj] = *reinterpret_cast<const double2*>(sb + rowB + nj * 8 * 16 + offB[p]);
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int nj = 0; nj < J; ++nj) dmma884(acc.v[mi][nj][0], acc.v[mi][nj][1], a2[mi].x, b2[nj].x);
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int nj = 0; nj < J; ++nj) dmma884(acc.v[mi][nj][0], acc.v[mi][nj][1], a2[mi].y, b2[nj].y);
       }
+    } else {
 #pragma unroll
-      for (int nj = 0; nj < J; ++nj) {
-        const int col = wn * 8 * J + nj * 8 + r8;
-        if (!MM) {
-          bf[nj] = sb[swz128(col, s * 4 + c4)];
-        } else {
-          const int k = s + 4 * c4;
-          bf[nj] = sb[(col >> 4) * (16 * BK) + swz128(k, col & 15)];
+      for (int s = 0; s < 4; ++s) {
+        double af[4], bf[J];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+          af[mi] = sa[mmA[s][mi]];
+          if (CHECK) bad |= is_nonfinite(af[mi]);
         }
-      }
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) {
-        if (mi < mvf) {
-#pragma unroll
-          for (int nj = 0; nj < J; ++nj)
-            if (nj < nvf) dmma884(acc.v[mi][nj][0], acc.v[mi][nj][1], af[mi], bf[nj]);
+        for (int nj = 0; nj < J; ++nj) {
+          const int col = wn * 8 * J + nj * 8 + r8;
+          bf[nj] = sb[(col >> 4) * (16 * BK) + mmB[s] + (((((col & 15) >> 1) ^ ((s + 4 * c4) & 7)) << 1) | (col & 1))];
         }
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int nj = 0; nj < J; ++nj) dmma884(acc.v[mi][nj][0], acc.v[mi][nj][1], af[mi], bf[nj]);
       }
     }
     __syncwarp();

@@ -1,4 +1,5 @@
 set -x
-python tools/prof_gemm.py 16384 > gpurun_out/prof_plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 20 --csv --log-file gpurun_out/launches_gemm.csv python tools/prof_gemm.py 16384 > gpurun_out/ncu_list.log 2>&1
-ncu --set full --clock-control none --import-source on -s 4 -c 1 -o gpurun_out/prof_gemm_kk python tools/prof_gemm.py 16384 > gpurun_out/ncu_gemm.log 2>&1
-nvidia-smi --help-query-gpu | grep -i -A2 "reasons.active" | head -8 > gpurun_out/smi_help.log
+python -m pytest tests -m gpu -x -q 2>&1 | tail -5 > gpurun_out/gputest3.log
+python tools/debug_gpu.py 2>&1 | tail -8 > gpurun_out/debug3.log
+python bench.py --steps 3 --warmup 2 --no-rpca --no-e2e --no-cpu 2>&1 | tail -1 > gpurun_out/bench_c3b.log
+python bench.py --workload c2 --steps 10 --warmup 3 --no-rpca --no-e2e --no-cpu 2>&1 | tail -1 > gpurun_out/bench_c2b.log
