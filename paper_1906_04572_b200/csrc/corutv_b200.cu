@@ -21,6 +21,7 @@
 #include "aux.cuh"
 #include "common.cuh"
 #include "gemm.cuh"
+#include "qrcp_cluster.cuh"
 #include "small.cuh"
 
 #define CORUTV_VERSION 100
@@ -407,10 +408,13 @@ struct QrJob {
 void cholqr_multi(corutv_handle* h, QrJob* jobs, int njobs, int ell, int64_t ldx,
                   const double* extra_flag = nullptr) {
   const int l = ell;
-  const size_t wbytes = (size_t)l * l * 8;
   const int optin = max_optin_smem(h);
-  const bool smem = wbytes + 8 * 1024 <= (size_t)optin - 8 * 1024;
-  if (smem) set_smem(h, small::chol_factor_kernel, wbytes);
+  const size_t static_smem = 4096;
+  const size_t aug = 2 * (size_t)l * l * 8;               // [G | I] in shared memory
+  const size_t stage = (size_t)small::NB * (l + small::NB) * 8;  // panel staging (global mode)
+  const bool smem = aug + static_smem <= (size_t)optin;
+  const size_t wbytes = smem ? aug : stage;
+  set_smem(h, small::chol_factor_kernel, wbytes);
   for (int step = 0; step < kMaxQrSteps; ++step) {
     int active = 0;
     for (int j = 0; j < njobs; ++j) {
@@ -420,7 +424,7 @@ void cholqr_multi(corutv_handle* h, QrJob* jobs, int njobs, int ell, int64_t ldx
       const double coeff = 11.0 * (q.rows_global * l + (double)l * (l + 1)) * kUnit;
       run_gemm(h, true, l, l, q.rows, q.cur, ldx, q.cur, ldx, q.w.G, ldx, nullptr, 0, q.w.ws);
       if (q.sharded) allreduce(h, q.w.G, (int64_t)l * ldx);
-      small::chol_factor_kernel<<<1, small::THREADS, smem ? wbytes : 0, h->stream>>>(
+      small::chol_factor_kernel<<<1, 512, wbytes, h->stream>>>(
           q.w.G, l, ldx, coeff, 1, kKappaPlain, q.w.rinvT, ldx, q.w.gwork, smem ? 1 : 0, q.w.info);
       CK_LAUNCH();
       run_gemm(h, false, q.rows, l, l, q.cur, ldx, q.w.rinvT, ldx, q.nxt, ldx, nullptr, 0, q.w.ws);
@@ -462,24 +466,61 @@ double* cholqr(corutv_handle* h, double* xa, double* xb, int64_t rows, int ell, 
 }
 
 // --------------------------------------------------------------- QRCP
+// l <= 32: one CTA (qrcp_kernel).  Larger cores: the thread-block-cluster
+// kernel (qrcp_cluster.cuh) with the core spread over CS CTAs' shared memory.
 void qrcp(corutv_handle* h, const double* D, int l, int64_t ldd, double* T, int64_t ldt, double* qtT,
           int64_t ldq, long long* perm_out, int* perm32, double* gwork) {
   const int optin = max_optin_smem(h);
-  const size_t stat = 6 * small::LMAX * 8 + 1024;
-  const size_t one = (size_t)l * l * 8;
-  int smR = 0, smQ = 0;
-  size_t dyn = 0;
-  if (2 * one + stat <= (size_t)optin) {
-    smR = smQ = 1;
-    dyn = 2 * one;
-  } else if (one + stat <= (size_t)optin) {
-    smR = 1;
-    dyn = one;
+  if (l <= 32) {
+    const size_t stat = 5 * small::LMAX * 8 + 4 * small::LMAX * 4 + 1024;
+    const size_t one = (size_t)l * l * 8;
+    int smR = 0, smQ = 0;
+    size_t dyn = 0;
+    if (2 * one + stat <= (size_t)optin) {
+      smR = smQ = 1;
+      dyn = 2 * one;
+    } else if (one + stat <= (size_t)optin) {
+      smR = 1;
+      dyn = one;
+    }
+    if (dyn) set_smem(h, small::qrcp_kernel, dyn);
+    small::qrcp_kernel<<<1, 1024, dyn, h->stream>>>(D, l, ldd, T, ldt, qtT, ldq, perm_out, perm32, gwork,
+                                                     smR, smQ);
+    CK_LAUNCH();
+    return;
   }
-  if (dyn) set_smem(h, small::qrcp_kernel, dyn);
-  small::qrcp_kernel<<<1, small::THREADS, dyn, h->stream>>>(D, l, ldd, T, ldt, qtT, ldq, perm_out, perm32,
-                                                            gwork, smR, smQ);
-  CK_LAUNCH();
+  // cluster size: enough CTAs that R (and Q when possible) fit on chip
+  const size_t stat = sizeof(qc::Shared) + 1024;
+  int cs = 2;
+  for (; cs <= 16; cs *= 2) {
+    const int cw = (l + cs - 1) / cs;
+    if ((size_t)cw * l * 8 * 2 + stat <= (size_t)optin) break;  // R and Q on chip
+  }
+  bool q_smem = true;
+  if (cs > 16) {
+    cs = 16;
+    q_smem = false;
+  }
+  const int cw = (l + cs - 1) / cs;
+  const size_t dyn = (size_t)cw * l * 8 * (q_smem ? 2 : 1);
+  if (dyn + stat > (size_t)optin) fail(h, CORUTV_ERR_ARG, "QRCP core too large for a 16-CTA cluster");
+  CK(cudaFuncSetAttribute(qc::qrcp_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+  if (cs > 8) CK(cudaFuncSetAttribute(qc::qrcp_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs, 1, 1);
+  cfg.blockDim = dim3(qc::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = dyn;
+  cfg.stream = h->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, qc::qrcp_cluster_kernel, D, l, ldd, cw, T, ldt, qtT, ldq, perm_out, perm32,
+                        gwork, q_smem ? 1 : 0));
+  ++h->launches;
 }
 
 // one-sided Jacobi: singular values of the matrix whose columns are the nv
@@ -489,10 +530,11 @@ void jacobi(corutv_handle* h, const double* X, int nv, int len, int64_t ldx, dou
   const int n = nv + (nv > 1 && (nv & 1));
   const size_t bytes = ((size_t)n * len + (pinv ? (size_t)n * n : 0)) * 8;
   const int optin = max_optin_smem(h);
-  const size_t stat = (small::LMAX * 2 + small::LMAX) * 8 + 8 * 1024;
+  const size_t stat = (small::LMAX * 2) * 8 + 8 * 1024;
   const bool smem = bytes + stat <= (size_t)optin;
   if (smem) set_smem(h, small::jacobi_kernel, bytes);
-  small::jacobi_kernel<<<1, small::THREADS, smem ? bytes : 0, h->stream>>>(
+  const int jt = (int)std::min<int64_t>(1024, std::max<int64_t>(64, 32 * (int64_t)((n + 1) / 2)));
+  small::jacobi_kernel<<<1, jt, smem ? bytes : 0, h->stream>>>(
       X, nv, len, ldx, 1e-14, 100, sig, pinv, ldp, gwork, smem ? 1 : 0, status);
   CK_LAUNCH();
 }

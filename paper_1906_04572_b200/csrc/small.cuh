@@ -27,7 +27,7 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   __syncthreads();
   double t = 0.0;
   if (threadIdx.x < 32) {
-    t = (lane < NWARPS) ? red[lane] : 0.0;
+    t = (lane < (int)(blockDim.x >> 5)) ? red[lane] : 0.0;
     t = warp_sum(t);
     if (lane == 0) red[0] = t;
   }
@@ -45,108 +45,217 @@ struct CholInfo {
   double trace;
 };
 
-// Returns true on failure.  W holds G's upper triangle (row-major, ld l).
-__device__ bool chol_upper_inplace(double* W, int l, double* red) {
-  for (int j = 0; j < l; ++j) {
-    __syncthreads();
-    const double d = W[j * l + j];
-    if (!(d > 0.0) || !isfinite(d)) return true;
-    const double r = sqrt(d);
-    for (int k = j + 1 + threadIdx.x; k < l; k += THREADS) W[j * l + k] = W[j * l + k] / r;
-    __syncthreads();
-    if (threadIdx.x == 0) W[j * l + j] = r;
-    const int T = l - j - 1;
-    for (int idx = threadIdx.x; idx < T * T; idx += THREADS) {
-      const int i = j + 1 + idx / T, k = j + 1 + idx % T;
-      if (k >= i) W[i * l + k] -= W[j * l + i] * W[j * l + k];
+// Blocked Cholesky of the augmented matrix [G | I] (row-major, ld = 2l):
+// the row operations that turn G into R (R'R = G) turn I into R^-T, so the
+// right half ends up holding rinvT[j][k] = R^-1[k][j] -- exactly the Bt
+// operand of the X * R^-1 GEMM -- without a separate triangular inverse.
+// Panels of NB rows: (a) one warp factors the NB x NB diagonal block,
+// (b) thread-per-column forward substitution applies D^-T to the panel's
+// rows (left trailing columns + right-half columns 0..kb+nb-1), (c) the
+// trailing rows get the Schur update in 4 x 4 register tiles (upper
+// triangle on the left, lower-triangular nonzero band on the right).
+// W may be shared or global memory (generic pointer); in global mode the
+// panel rows are staged in shared memory (`stage`).
+constexpr int NB = 32;
+
+__device__ __forceinline__ void tile_update(double* W, int ld, const double* P, int pld,
+                                            int pcol0, int nb, int i0, int k0, int imax,
+                                            int kmax, bool upper, int roff) {
+  // W[i][k] -= sum_p P[p][i - pcol0] * P[p][k - pcol0 + roff] for the 4x4 tile
+  double acc[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+  for (int p = 0; p < nb; ++p) {
+    const double* row = P + (int64_t)p * pld;
+    double a[4], b[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) a[r] = (i0 + r < imax) ? row[i0 + r - pcol0] : 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) b[c] = (k0 + c < kmax) ? row[k0 + c - pcol0 + roff] : 0.0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[r][c] = fma(a[r], b[c], acc[r][c]);
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int i = i0 + r;
+    if (i >= imax) continue;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int k = k0 + c;
+      if (k >= kmax || (upper && k < i)) continue;
+      W[(int64_t)i * ld + k + (upper ? 0 : roff)] -= acc[r][c];
     }
   }
-  __syncthreads();
+}
+
+// Returns true on failure (non-positive / non-finite pivot), uniformly.
+__device__ bool chol_aug_blocked(double* W, int l, bool wglobal, double* stage, int* s_flag) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int ld = 2 * l;
+  for (int kb = 0; kb < l; kb += NB) {
+    const int nb = min(NB, l - kb);
+    // (a) diagonal block, warp 0 (lane = column inside the block)
+    if (warp == 0) {
+      int bad = 0;
+      for (int j = 0; j < nb; ++j) {
+        const double d = W[(int64_t)(kb + j) * ld + kb + j];
+        if (!(d > 0.0) || !isfinite(d)) { bad = 1; break; }
+        const double r = sqrt(d);
+        __syncwarp();
+        if (lane > j && lane < nb) W[(int64_t)(kb + j) * ld + kb + lane] /= r;
+        __syncwarp();
+        if (lane == j) W[(int64_t)(kb + j) * ld + kb + j] = r;
+        if (lane > j && lane < nb) {
+          const double f = W[(int64_t)(kb + j) * ld + kb + lane];
+          for (int i = j + 1; i <= lane; ++i)
+            W[(int64_t)(kb + i) * ld + kb + lane] -= W[(int64_t)(kb + j) * ld + kb + i] * f;
+        }
+        __syncwarp();
+      }
+      if (lane == 0) *s_flag = bad;
+    }
+    __syncthreads();
+    if (*s_flag) return true;
+    // (b) rows kb..kb+nb  <-  D^-T rows, for left columns [kb+nb, l) and right
+    //     columns [l, l + kb + nb)
+    const int c0 = kb + nb;
+    const int nleft = l - c0, nright = kb + nb;
+    for (int t = tid; t < nleft + nright; t += nt) {
+      const int c = (t < nleft) ? c0 + t : l + (t - nleft);
+      double x[NB];
+#pragma unroll
+      for (int i = 0; i < NB; ++i) x[i] = (i < nb) ? W[(int64_t)(kb + i) * ld + c] : 0.0;
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        if (i < nb) {
+          double sacc = x[i];
+#pragma unroll
+          for (int q = 0; q < i; ++q) sacc -= W[(int64_t)(kb + q) * ld + kb + i] * x[q];
+          x[i] = sacc / W[(int64_t)(kb + i) * ld + kb + i];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+        if (i < nb) W[(int64_t)(kb + i) * ld + c] = x[i];
+    }
+    __syncthreads();
+    if (c0 >= l) break;
+    // stage the panel rows (columns [c0, l) and [l, l + nright)) for global W
+    const double* P = W + (int64_t)kb * ld;
+    int pld = ld, pcol0 = 0;
+    if (wglobal) {
+      const int w = nleft + nright;
+      for (int p = warp; p < nb; p += nt >> 5)
+        for (int c = lane; c < w; c += 32) stage[p * w + c] = W[(int64_t)(kb + p) * ld + c0 + c];
+      __syncthreads();
+      P = stage;
+      pld = w;
+      pcol0 = c0;
+    }
+    // (c) trailing rows i in [c0, l):
+    //     left  : W[i][k] -= sum_p P[p][i] P[p][k],   i <= k < l
+    //     right : W[i][l + k'] -= sum_p P[p][i] P[p][l + k'],  k' < nright
+    const int TI = (nleft + 3) / 4;
+    const int nup = TI * (TI + 1) / 2;        // upper-triangle 4x4 tiles
+    const int TR = (nright + 3) / 4;
+    const int nrt = TI * TR;                  // right-half tiles
+    // global columns of the staged right part start at pcol0 + nleft
+    const int roff = wglobal ? (nleft - (l - c0)) : 0;  // == 0 by construction
+    for (int t = tid; t < nup + nrt; t += nt) {
+      if (t < nup) {
+        int tk = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+        while ((tk + 1) * (tk + 2) / 2 <= t) ++tk;
+        while (tk * (tk + 1) / 2 > t) --tk;
+        const int ti = t - tk * (tk + 1) / 2;
+        tile_update(W, ld, P, pld, pcol0, nb, c0 + 4 * ti, c0 + 4 * tk, l, l, true, 0);
+      } else {
+        const int u = t - nup;
+        const int ti = u / TR, tk = u % TR;
+        // right-half column k' lives at W column l + k' and staged column
+        // (l - c0) + k' (global mode) or l + k' (shared mode)
+        tile_update(W, ld, P, pld, pcol0, nb, c0 + 4 * ti, l + 4 * tk, l, l + nright, false, roff);
+      }
+    }
+    __syncthreads();
+  }
   return false;
 }
 
-__device__ double upper_sumsq(const double* W, int l, double* red) {
+__device__ double upper_sumsq(const double* W, int l, int ld, int col0, bool lower, double* red) {
   double s = 0.0;
-  for (int idx = threadIdx.x; idx < l * l; idx += THREADS) {
-    const int i = idx / l, k = idx % l;
-    if (k >= i) s += W[idx] * W[idx];
-  }
-  return block_sum(s, red);
-}
-
-// In-place inverse of an upper-triangular matrix, column by column.
-__device__ void inv_upper_inplace(double* W, int l, double* tmp) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int j = 0; j < l; ++j) {
-    __syncthreads();
-    const double invd = 1.0 / W[j * l + j];
-    for (int i = warp; i < j; i += NWARPS) {
-      double s = 0.0;
-      for (int k = i + lane; k < j; k += 32) s += W[i * l + k] * W[k * l + j];
-      s = warp_sum(s);
-      if (lane == 0) tmp[i] = -s * invd;
+  for (int i = threadIdx.x >> 5; i < l; i += blockDim.x >> 5)
+    for (int k = threadIdx.x & 31; k < l; k += 32) {
+      if (lower ? (k > i) : (k < i)) continue;
+      const double v = W[(int64_t)i * ld + col0 + k];
+      s += v * v;
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < j; i += THREADS) W[i * l + j] = tmp[i];
-    if (threadIdx.x == 0) W[j * l + j] = invd;
-  }
-  __syncthreads();
+  return block_sum(s, red);
 }
 
 // G: l x l (ld ldg).  shift_coeff = 11 (m l + l (l + 1)) u  (shifted
 // CholeskyQR, Fukaya et al. 2020).  allow_plain: try the unshifted factor
 // first and keep it when it succeeds with kappa_F <= kappa_max.
 // Output rinvT (l x l, ld ldr): rinvT[j][k] = R^-1[k][j] (the Bt operand of
-// the X * R^-1 GEMM).
-__global__ void __launch_bounds__(THREADS, 1)
+// the X * R^-1 GEMM).  Work: [G | I], 2 l^2 doubles (shared or global).
+__global__ void __launch_bounds__(512, 1)
     chol_factor_kernel(const double* __restrict__ G, int l, int64_t ldg, double shift_coeff,
                        int allow_plain, double kappa_max, double* __restrict__ rinvT,
                        int64_t ldr, double* gwork, int use_smem, CholInfo* info) {
   extern __shared__ double dsm[];
   __shared__ double red[NWARPS];
-  __shared__ double tmp[LMAX];
+  __shared__ int s_flag;
   double* W = use_smem ? dsm : gwork;
+  double* stage = use_smem ? nullptr : dsm;
+  const int ld = 2 * l;
   double tr = 0.0;
-  for (int i = threadIdx.x; i < l; i += THREADS) tr += G[i * ldg + i];
+  for (int i = threadIdx.x; i < l; i += blockDim.x) tr += G[i * ldg + i];
   tr = block_sum(tr, red);
   int shifted = allow_plain ? 0 : 1;
   int status = 0;
   double kappa = 0.0;
   if (!(tr > 0.0) || !isfinite(tr)) {
     // exactly zero sketch (or garbage): R = I, Q = X.
-    for (int idx = threadIdx.x; idx < l * l; idx += THREADS) W[idx] = (idx / l == idx % l) ? 1.0 : 0.0;
+    for (int i = threadIdx.x >> 5; i < l; i += blockDim.x >> 5)
+      for (int k = threadIdx.x & 31; k < l; k += 32) W[(int64_t)i * ld + l + k] = (i == k) ? 1.0 : 0.0;
     status = isfinite(tr) ? 1 : 2;
     kappa = 1.0;
     __syncthreads();
   } else {
     for (;;) {
       const double s = shifted ? shift_coeff * tr : 0.0;
-      for (int idx = threadIdx.x; idx < l * l; idx += THREADS) {
-        const int i = idx / l, k = idx % l;
-        double g = (k >= i) ? G[i * ldg + k] : 0.0;
-        if (i == k) g += s;
-        W[idx] = g;
-      }
+      for (int i = threadIdx.x >> 5; i < l; i += blockDim.x >> 5)
+        for (int k = threadIdx.x & 31; k < 2 * l; k += 32) {
+          double g;
+          if (k < l) {
+            g = (k >= i) ? G[i * ldg + k] : 0.0;
+            if (i == k) g += s;
+          } else {
+            g = (k - l == i) ? 1.0 : 0.0;
+          }
+          W[(int64_t)i * ld + k] = g;
+        }
       __syncthreads();
-      const bool fail = chol_upper_inplace(W, l, red);
+      const bool fail = chol_aug_blocked(W, l, !use_smem, stage, &s_flag);
+      __syncthreads();
       if (fail) {
-        if (!shifted) { shifted = 1; __syncthreads(); continue; }
+        if (!shifted) { shifted = 1; continue; }
         status = 2;
         break;
       }
-      const double nr = upper_sumsq(W, l, red);
-      inv_upper_inplace(W, l, tmp);
-      const double ni = upper_sumsq(W, l, red);
+      const double nr = upper_sumsq(W, l, ld, 0, false, red);
+      const double ni = upper_sumsq(W, l, ld, l, true, red);
       kappa = sqrt(nr) * sqrt(ni);
       if (!shifted && !(kappa <= kappa_max)) { shifted = 1; __syncthreads(); continue; }
       break;
     }
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < l * l; idx += THREADS) {
-    const int k = idx / l, j = idx % l;  // rinvT[j][k] = Rinv[k][j]
-    rinvT[j * ldr + k] = (j >= k) ? W[k * l + j] : 0.0;
-  }
+  for (int j = threadIdx.x >> 5; j < l; j += blockDim.x >> 5)  // rinvT = right half (lower)
+    for (int k = threadIdx.x & 31; k < l; k += 32) rinvT[j * ldr + k] = (k <= j) ? W[(int64_t)j * ld + l + k] : 0.0;
   if (threadIdx.x == 0) {
     info->shifted = shifted;
     info->status = status;
@@ -158,159 +267,185 @@ __global__ void __launch_bounds__(THREADS, 1)
 // ------------------------------------------------------------------- QRCP
 // D: l x l (ld ldd).  Outputs: T (ld ldt) = triu(R); qtT (ld ldq):
 // qtT[j][i] = Q[i][j]; perm (int64) and perm32.
-// WR / WQ: l x l work (smem or global).  Small per-column state lives in
-// static shared arrays of LMAX.
+//
+// Businger-Golub exactly as dense.py:152-192, organised for one CTA with a
+// single barrier per pivot step: columns never move physically (a
+// logical->physical map is double-buffered by step parity, so the
+// lowest-LOGICAL-index tie-break of dense.py:169 is kept), every warp
+// redundantly computes the pivot argmax and the reflector norm (no barrier
+// needed to broadcast them), and a group of G lanes owns each physical
+// column: it forms the column's reflector coefficient (G-way split dot +
+// shuffle reduction), applies the update and downdates / refreshes the
+// column norm (dense.py:181-190).  The new diagonal goes to diag[] so the
+// pivot column stays read-only within a step.  R / Q live in shared memory
+// when they fit (smem_R / smem_Q), else in L2-resident global scratch.
+template <int G>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int G>
+__device__ void qrcp_body(double* R, double* Q, int l, double* nrm, double* ref, double* tau,
+                          double* vhead, double* diag, int (*l2p)[LMAX], int* done, int* has_ref,
+                          const int** fin_out) {
+  const int lane = threadIdx.x & 31;
+  const int nt = blockDim.x;
+  const int gid = threadIdx.x / G, gl = threadIdx.x % G;
+  const int ngroups = nt / G;
+  for (int j = 0; j < l; ++j) {
+    const int* cur = l2p[j & 1];
+    int* nxt = l2p[(j + 1) & 1];
+    // pivot = first logical position of the max downdated norm (every warp)
+    double best = -1.0;
+    int bq = l;
+    for (int q = j + lane; q < l; q += 32) {
+      const double v = nrm[cur[q]];
+      if (v > best) { best = v; bq = q; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
+      if (ov > best || (ov == best && oq < bq)) { best = ov; bq = oq; }
+    }
+    const int p = bq;
+    const int pc = cur[p];
+    // reflector of x = R[j:, pc] (dense.py:104-114), every warp
+    const double x0 = R[j * l + pc];
+    double t2 = 0.0;
+    for (int i = j + 1 + lane; i < l; i += 32) t2 += R[i * l + pc] * R[i * l + pc];
+    t2 = warp_sum(t2);
+    const double nx = sqrt(x0 * x0 + t2);
+    const bool refl = nx != 0.0;
+    const double v0 = refl ? x0 + (x0 >= 0.0 ? nx : -nx) : 0.0;
+    const double tj = refl ? 2.0 / (v0 * v0 + t2) : 0.0;
+    for (int q = threadIdx.x; q < l; q += nt) nxt[q] = (q == j) ? cur[p] : ((q == p) ? cur[j] : cur[q]);
+    if (threadIdx.x == 0) {
+      diag[j] = refl ? x0 - v0 * (tj * (v0 * x0 + t2)) : x0;
+      tau[j] = tj;
+      vhead[j] = v0;
+      has_ref[j] = refl;
+    }
+    // apply H_j to the other active columns: group per physical column
+    for (int cb = 0; cb < l; cb += ngroups) {
+      const int c = cb + gid;
+      const bool act = c < l && c != pc && !done[c];
+      const int cc = act ? c : pc;  // inactive lanes read a valid column
+      double s = 0.0;
+      if (refl) {
+        for (int i = j + 1 + gl; i < l; i += G) s += R[i * l + pc] * R[i * l + cc];
+        if (gl == 0) s += v0 * R[j * l + cc];
+        s = group_sum<G>(s);
+        const double w = tj * s;
+        if (act) {
+          for (int i = j + 1 + gl; i < l; i += G) R[i * l + c] -= R[i * l + pc] * w;
+          if (gl == 0) R[j * l + c] -= v0 * w;
+        }
+      }
+      // norm downdate (dense.py:181-185), refresh when stale (dense.py:185-190)
+      double nv = 0.0;
+      bool stale = false;
+      if (act && j + 1 < l) {
+        const double rj = R[j * l + c];  // gl == 0 wrote it; same lane reads
+        nv = fmax(nrm[c] - rj * rj, 0.0);
+        stale = nv < 1e-10 * ref[c];
+      }
+      stale = __shfl_sync(0xffffffffu, stale ? 1 : 0, (lane / G) * G) != 0;
+      if (__any_sync(0xffffffffu, stale)) {
+        double f = 0.0;
+        for (int i = j + 1 + gl; i < l; i += G) f += R[i * l + cc] * R[i * l + cc];
+        f = group_sum<G>(f);
+        if (stale) nv = f;
+        if (stale && gl == 0) ref[c] = f;
+      }
+      if (act && gl == 0 && j + 1 < l) nrm[c] = nv;
+    }
+    if (threadIdx.x == 0) done[pc] = 1;
+    __syncthreads();
+  }
+  const int* fin = l2p[l & 1];
+  *fin_out = fin;
+
+  // explicit Q by reverse accumulation on the identity (dense.py:117-129)
+  for (int i = threadIdx.x >> 5; i < l; i += nt >> 5)
+    for (int c = lane; c < l; c += 32) Q[i * l + c] = (i == c) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int j = l - 1; j >= 0; --j) {
+    if (has_ref[j]) {
+      const int pc = fin[j];
+      const double v0 = vhead[j], tj = tau[j];
+      for (int cb = j; cb < l; cb += ngroups) {
+        const int c = cb + gid;
+        const bool act = c < l;
+        const int cc = act ? c : j;
+        double s = 0.0;
+        for (int i = j + 1 + gl; i < l; i += G) s += R[i * l + pc] * Q[i * l + cc];
+        if (gl == 0) s += v0 * Q[j * l + cc];
+        s = group_sum<G>(s);
+        const double w = tj * s;
+        if (act) {
+          for (int i = j + 1 + gl; i < l; i += G) Q[i * l + c] -= R[i * l + pc] * w;
+          if (gl == 0) Q[j * l + c] -= v0 * w;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
     qrcp_kernel(const double* __restrict__ D, int l, int64_t ldd, double* __restrict__ T,
                 int64_t ldt, double* __restrict__ qtT, int64_t ldq, long long* perm_out,
                 int* perm32, double* gwork, int smem_R, int smem_Q) {
   extern __shared__ double dsm[];
-  __shared__ double red[NWARPS];
   __shared__ double nrm[LMAX];
   __shared__ double ref[LMAX];
   __shared__ double tau[LMAX];
   __shared__ double vhead[LMAX];
-  __shared__ int perm[LMAX];
+  __shared__ double diag[LMAX];
+  __shared__ int l2p[2][LMAX];
+  __shared__ int done[LMAX];
   __shared__ int has_ref[LMAX];
-  __shared__ int piv_idx[NWARPS];
-  __shared__ double piv_val[NWARPS];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nt = blockDim.x;
   double* R = smem_R ? dsm : gwork;
   double* Q = smem_Q ? (smem_R ? dsm + l * l : dsm) : gwork + (int64_t)l * l;
 
-  for (int idx = threadIdx.x; idx < l * l; idx += THREADS) R[idx] = D[(idx / l) * ldd + idx % l];
+  for (int i = threadIdx.x >> 5; i < l; i += nt >> 5)
+    for (int c = lane; c < l; c += 32) R[i * l + c] = D[i * ldd + c];
   __syncthreads();
   // initial column norms^2 (dense.py:165-166)
-  for (int c = warp; c < l; c += NWARPS) {
+  for (int c = threadIdx.x >> 5; c < l; c += nt >> 5) {
     double s = 0.0;
     for (int i = lane; i < l; i += 32) s += R[i * l + c] * R[i * l + c];
     s = warp_sum(s);
-    if (lane == 0) { nrm[c] = s; ref[c] = s; perm[c] = c; }
+    if (lane == 0) {
+      nrm[c] = s;
+      ref[c] = s;
+      l2p[0][c] = c;
+      done[c] = 0;
+    }
   }
   __syncthreads();
-
-  for (int j = 0; j < l; ++j) {
-    // pivot: argmax nrm[j:], first index on ties (dense.py:169)
-    double best = -1.0;
-    int bi = l;
-    for (int c = j + threadIdx.x; c < l; c += THREADS) {
-      const double v = nrm[c];
-      if (v > best) { best = v; bi = c; }  // increasing c: keeps first max
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-    }
-    if (lane == 0) { piv_val[warp] = best; piv_idx[warp] = bi; }
-    __syncthreads();
-    if (warp == 0) {
-      best = piv_val[lane];
-      bi = piv_idx[lane];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-      }
-      if (lane == 0) piv_idx[0] = bi;
-    }
-    __syncthreads();
-    const int p = piv_idx[0];
-    if (p != j) {
-      for (int i = threadIdx.x; i < l; i += THREADS) {
-        const double t = R[i * l + j];
-        R[i * l + j] = R[i * l + p];
-        R[i * l + p] = t;
-      }
-      if (threadIdx.x == 0) {
-        int ti = perm[j]; perm[j] = perm[p]; perm[p] = ti;
-        double t = nrm[j]; nrm[j] = nrm[p]; nrm[p] = t;
-        t = ref[j]; ref[j] = ref[p]; ref[p] = t;
-      }
-    }
-    __syncthreads();
-    // reflector of x = R[j:, j] (dense.py:104-114)
-    double part = 0.0;
-    for (int i = j + threadIdx.x; i < l; i += THREADS) part += R[i * l + j] * R[i * l + j];
-    const double nx2 = block_sum(part, red);
-    const double x0 = R[j * l + j];
-    __syncthreads();  // x0 is overwritten below by the warp owning column j
-    const bool refl = (sqrt(nx2) != 0.0);
-    double v0 = 0.0, tj = 0.0;
-    if (refl) {
-      const double nx = sqrt(nx2);
-      v0 = x0 + (x0 >= 0.0 ? nx : -nx);
-      // v'v = v0^2 + sum_{i>j} x_i^2
-      tj = 2.0 / (v0 * v0 + (nx2 - x0 * x0));
-    }
-    if (threadIdx.x == 0) { has_ref[j] = refl; tau[j] = tj; vhead[j] = v0; }
-    // apply H to columns c >= j; warp per column.  Column j keeps v below
-    // the diagonal (LAPACK-style storage); only its diagonal is updated.
-    if (refl) {
-      for (int c = j + warp; c < l; c += NWARPS) {
-        double s = (lane == 0) ? v0 * R[j * l + c] : 0.0;
-        for (int i = j + 1 + lane; i < l; i += 32) s += R[i * l + j] * R[i * l + c];
-        s = warp_sum(s);
-        const double w = tj * s;
-        if (c == j) {
-          if (lane == 0) R[j * l + j] = x0 - v0 * w;
-        } else {
-          for (int i = j + 1 + lane; i < l; i += 32) R[i * l + c] -= R[i * l + j] * w;
-          if (lane == 0) R[j * l + c] -= v0 * w;
-        }
-      }
-    }
-    __syncthreads();
-    // norm downdate + exact refresh of stale norms (dense.py:181-190)
-    if (j + 1 < l) {
-      for (int c = j + 1 + warp; c < l; c += NWARPS) {
-        double nv = 0.0;
-        if (lane == 0) {
-          const double rj = R[j * l + c];
-          nv = nrm[c] - rj * rj;
-          nv = fmax(nv, 0.0);
-        }
-        nv = __shfl_sync(0xffffffffu, nv, 0);
-        if (nv < 1e-10 * ref[c]) {
-          double s = 0.0;
-          for (int i = j + 1 + lane; i < l; i += 32) s += R[i * l + c] * R[i * l + c];
-          s = warp_sum(s);
-          if (lane == 0) { nrm[c] = s; ref[c] = s; }
-        } else if (lane == 0) {
-          nrm[c] = nv;
-        }
-      }
-    }
-    __syncthreads();
-  }
-
-  // explicit Q by reverse accumulation on the identity (dense.py:117-129)
-  for (int idx = threadIdx.x; idx < l * l; idx += THREADS) Q[idx] = (idx / l == idx % l) ? 1.0 : 0.0;
+  const int* fin = nullptr;
+  const int per = nt / l;  // lanes available per column
+  if (per >= 32) qrcp_body<32>(R, Q, l, nrm, ref, tau, vhead, diag, l2p, done, has_ref, &fin);
+  else if (per >= 16) qrcp_body<16>(R, Q, l, nrm, ref, tau, vhead, diag, l2p, done, has_ref, &fin);
+  else if (per >= 8) qrcp_body<8>(R, Q, l, nrm, ref, tau, vhead, diag, l2p, done, has_ref, &fin);
+  else if (per >= 4) qrcp_body<4>(R, Q, l, nrm, ref, tau, vhead, diag, l2p, done, has_ref, &fin);
+  else if (per >= 2) qrcp_body<2>(R, Q, l, nrm, ref, tau, vhead, diag, l2p, done, has_ref, &fin);
+  else qrcp_body<4>(R, Q, l, nrm, ref, tau, vhead, diag, l2p, done, has_ref, &fin);
   __syncthreads();
-  for (int j = l - 1; j >= 0; --j) {
-    if (has_ref[j]) {
-      const double v0 = vhead[j], tj = tau[j];
-      for (int c = j + warp; c < l; c += NWARPS) {
-        double s = (lane == 0) ? v0 * Q[j * l + c] : 0.0;
-        for (int i = j + 1 + lane; i < l; i += 32) s += R[i * l + j] * Q[i * l + c];
-        s = warp_sum(s);
-        const double w = tj * s;
-        for (int i = j + 1 + lane; i < l; i += 32) Q[i * l + c] -= R[i * l + j] * w;
-        if (lane == 0) Q[j * l + c] -= v0 * w;
-      }
+  for (int i = threadIdx.x >> 5; i < l; i += nt >> 5)
+    for (int c = lane; c < l; c += 32) {
+      T[i * ldt + c] = (c > i) ? R[i * l + fin[c]] : ((c == i) ? diag[i] : 0.0);
+      qtT[c * ldq + i] = Q[i * l + c];
     }
-    __syncthreads();
-  }
-  for (int idx = threadIdx.x; idx < l * l; idx += THREADS) {
-    const int i = idx / l, c = idx % l;
-    T[i * ldt + c] = (c >= i) ? R[idx] : 0.0;
-    qtT[c * ldq + i] = Q[idx];
-  }
-  for (int c = threadIdx.x; c < l; c += THREADS) {
-    if (perm_out) perm_out[c] = perm[c];
-    perm32[c] = perm[c];
+  for (int c = threadIdx.x; c < l; c += nt) {
+    if (perm_out) perm_out[c] = fin[c];
+    perm32[c] = fin[c];
   }
 }
 
@@ -318,30 +453,31 @@ __global__ void __launch_bounds__(THREADS, 1)
 // One-sided Jacobi on the nv rows (length len, ld ldx) of X: orthogonalises
 // them by plane rotations in the round-robin order of dense.py:200-210,
 // until every pair has |<xa,xb>| <= tol |xa||xb| (dense.py:223-282).
-// sig (device, nv, descending).  want_pinv: X holds B^T for an nv x nv ...
-// (general: B = X^T, len x nv); writes pinv(B) (nv x len, ld ldp) with the
-// cutoff max(len, nv) * sig0 * 1e-12 (dense.py:390-402).
+// One warp per pair (pairs of a round are disjoint), pairs computed
+// arithmetically by each warp, one barrier per round.
+// sig (device, nv, descending).  pinv != nullptr: B = X^T (len x nv) and
+// pinv(B) (nv x len, ld ldp) is written with the cutoff
+// max(len, nv) * sig0 * 1e-12 (dense.py:390-402).
 __global__ void __launch_bounds__(THREADS, 1)
     jacobi_kernel(const double* __restrict__ X, int nv, int len, int64_t ldx, double tol,
                   int max_sweeps, double* sig_out, double* pinv, int64_t ldp, double* gwork,
                   int use_smem, int* status) {
   extern __shared__ double dsm[];
-  __shared__ int pair_a[LMAX / 2 + 1], pair_b[LMAX / 2 + 1];
   __shared__ double offmax[NWARPS];
   __shared__ double sig[LMAX];
   __shared__ int order[LMAX];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int nt = blockDim.x;
   const int n = nv + (nv > 1 && (nv & 1));  // pad odd counts with a zero row
   const bool want_v = pinv != nullptr;
   double* W = use_smem ? dsm : gwork;          // n x len
   double* V = W + (int64_t)n * len;            // n x n (row a = column a of V)
-  for (int64_t idx = threadIdx.x; idx < (int64_t)n * len; idx += THREADS) {
-    const int r = idx / len, c = idx % len;
-    W[idx] = (r < nv) ? X[r * ldx + c] : 0.0;
-  }
+  for (int r = warp; r < n; r += nwarps)
+    for (int c = lane; c < len; c += 32) W[(int64_t)r * len + c] = (r < nv) ? X[r * ldx + c] : 0.0;
   if (want_v)
-    for (int64_t idx = threadIdx.x; idx < (int64_t)n * n; idx += THREADS)
-      V[idx] = (idx / n == idx % n) ? 1.0 : 0.0;
+    for (int r = warp; r < n; r += nwarps)
+      for (int c = lane; c < n; c += 32) V[(int64_t)r * n + c] = (r == c) ? 1.0 : 0.0;
   __syncthreads();
   int st = 0;
   if (n > 1) {
@@ -349,21 +485,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (; sweep < max_sweeps; ++sweep) {
       double off = 0.0;
       for (int round = 0; round < n - 1; ++round) {
-        // round-robin pairing: ring[0] fixed, others rotate
-        if (threadIdx.x < n / 2) {
-          const int t = threadIdx.x;
+        for (int pi = warp; pi < n / 2; pi += nwarps) {
+          // ring position -> player: position 0 fixed, the others rotate
           auto ring = [&](int pos) -> int {
             if (pos == 0) return 0;
             int q = (pos - 1 - round) % (n - 1);
             if (q < 0) q += n - 1;
             return 1 + q;
           };
-          pair_a[t] = ring(t);
-          pair_b[t] = ring(n - 1 - t);
-        }
-        __syncthreads();
-        for (int pi = warp; pi < n / 2; pi += NWARPS) {
-          const int a = pair_a[pi], b = pair_b[pi];
+          const int a = ring(pi), b = ring(n - 1 - pi);
           double* xa = W + (int64_t)a * len;
           double* xb = W + (int64_t)b * len;
           double al = 0.0, be = 0.0, ga = 0.0;
@@ -403,54 +533,45 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         __syncthreads();
       }
-      // block max of off
-      double m = off;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-      if (lane == 0) offmax[warp] = m;
+      if (lane == 0) offmax[warp] = off;
       __syncthreads();
-      if (threadIdx.x == 0) {
-        double mm = 0.0;
-        for (int w = 0; w < NWARPS; ++w) mm = fmax(mm, offmax[w]);
-        offmax[0] = mm;
-      }
+      double mm = 0.0;
+      for (int w = 0; w < nwarps; ++w) mm = fmax(mm, offmax[w]);
       __syncthreads();
-      const bool done = offmax[0] <= tol;
-      __syncthreads();
-      if (done) break;
+      if (mm <= tol) break;
     }
     if (sweep == max_sweeps) st = 1;
   }
   // singular values and stable descending order (dense.py:339-341)
-  for (int r = warp; r < nv; r += NWARPS) {
+  for (int r = warp; r < nv; r += nwarps) {
     double s = 0.0;
     for (int i = lane; i < len; i += 32) s += W[(int64_t)r * len + i] * W[(int64_t)r * len + i];
     s = warp_sum(s);
     if (lane == 0) sig[r] = sqrt(s);
   }
   __syncthreads();
-  for (int r = threadIdx.x; r < nv; r += THREADS) {
+  for (int r = threadIdx.x; r < nv; r += nt) {
     int rank = 0;
     for (int q = 0; q < nv; ++q) rank += (sig[q] > sig[r]) || (sig[q] == sig[r] && q < r);
     order[rank] = r;
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < nv; k += THREADS) sig_out[k] = sig[order[k]];
+  for (int k = threadIdx.x; k < nv; k += nt) sig_out[k] = sig[order[k]];
   if (want_v) {
     // B = X^T = U S V^T with U[:, k] = W[k] / sig_k.  pinv = V S^+ U^T.
     const double s0 = sig[order[0]];
     const double cut = (double)max(len, nv) * s0 * 1e-12;
-    for (int64_t idx = threadIdx.x; idx < (int64_t)nv * len; idx += THREADS) {
-      const int i = idx / len, j = idx % len;
-      double acc = 0.0;
-      if (s0 > 0.0) {
-        for (int k = 0; k < nv; ++k) {
-          const double sk = sig[k];
-          if (sk > cut) acc += V[(int64_t)k * n + i] * (W[(int64_t)k * len + j] / sk) / sk;
+    for (int i = warp; i < nv; i += nwarps)
+      for (int j = lane; j < len; j += 32) {
+        double acc = 0.0;
+        if (s0 > 0.0) {
+          for (int k = 0; k < nv; ++k) {
+            const double sk = sig[k];
+            if (sk > cut) acc += V[(int64_t)k * n + i] * (W[(int64_t)k * len + j] / sk) / sk;
+          }
         }
+        pinv[i * ldp + j] = acc;
       }
-      pinv[i * ldp + j] = acc;
-    }
   }
   if (threadIdx.x == 0 && status) *status = st;
 }
