@@ -72,6 +72,21 @@ int corutv_decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, in
                      int ell, int q_power, int variant, const double* omega, double* u, double* t,
                      double* v, int64_t* perm, int64_t* passes_host);
 
+/* Same, with the Gaussian test matrix drawn on the device from the PCG64
+ * state numpy's PCG64(seed) starts from: pcg_state = {state_hi, state_lo,
+ * inc_hi, inc_lo} (np.random.PCG64(seed).state, i.e. SeedSequence-expanded on
+ * the host).  Omega is bit-identical to gaussian_matrix(n, ell, seed)
+ * (sketch.py:63-68). */
+int corutv_decompose_seeded(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda,
+                            int ell, int q_power, int variant, const uint64_t* pcg_state, double* u,
+                            double* t, double* v, int64_t* perm, int64_t* passes_host);
+
+/* np.random.Generator(PCG64(seed)).standard_normal((rows, cols)) into out
+ * (row-major, ld) on the device, bit-identical (gaussian_matrix,
+ * sketch.py:63-68).  Synchronises the stream. */
+int corutv_gaussian(corutv_handle* h, const uint64_t* pcg_state, int64_t rows, int64_t cols,
+                    double* out, int64_t ld);
+
 /* Fused ALM update, rpca.py:211-216 with L = U[:, :r] (T[:r,:] V')
  * (rpca.py:129) formed tile-by-tile and never stored:
  *   g  = (M - L) + Y/mu ;  S = sign(g) max(|g| - lam/mu, 0)

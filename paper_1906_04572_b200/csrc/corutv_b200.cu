@@ -21,6 +21,12 @@
 #include "aux.cuh"
 #include "common.cuh"
 #include "gemm.cuh"
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
+
+#include "chol_cluster.cuh"
+#include "rng.cuh"
 #include "qrcp_cluster.cuh"
 #include "small.cuh"
 
@@ -35,6 +41,7 @@ struct corutv_handle {
   int rank = 0, world = 1;
   char* arena = nullptr;
   size_t arena_size = 0;
+  size_t arena_top = 0;  // Arena stack top (bytes)
   double* pinned = nullptr;  // 64 doubles of pinned host scratch
   int num_sms = 148;
   // profiling (corutv_profile_begin/end): launch counter always on; CUDA
@@ -114,10 +121,22 @@ struct TagScope {  // marks the GEMMs that sweep the data matrix (K1/K2/K5)
 };
 
 // ------------------------------------------------------------------ arena
+// Stack-disciplined workspace: an Arena carves its buffers from the handle's
+// block above the enclosing arena's top and releases them when it goes out of
+// scope.  Only the outermost arena may grow (re-allocate) the block; a nested
+// arena that does not fit takes a stream-ordered side allocation, so the
+// enclosing arena's pointers are never invalidated.
 struct Arena {
   corutv_handle* h;
-  size_t off = 0;
+  size_t base;
+  void* extra = nullptr;
+  bool committed = false;
   std::vector<std::pair<void**, size_t>> reqs;
+  explicit Arena(corutv_handle* hh) : h(hh), base(hh->arena_top) {}
+  ~Arena() {
+    if (committed) h->arena_top = base;
+    if (extra) cudaFreeAsync(extra, h->stream);
+  }
   template <typename T>
   void add(T** p, size_t count) {
     reqs.push_back({reinterpret_cast<void**>(p), round_up(count * sizeof(T), 256)});
@@ -125,7 +144,8 @@ struct Arena {
   void commit() {
     size_t total = 0;
     for (auto& r : reqs) total += r.second;
-    if (total > h->arena_size) {
+    char* mem = nullptr;
+    if (base == 0 && total > h->arena_size) {
       if (h->arena) {
         cudaStreamSynchronize(h->stream);
         cudaFree(h->arena);
@@ -139,9 +159,20 @@ struct Arena {
       }
       h->arena_size = want;
     }
+    if (base + total <= h->arena_size) {
+      mem = h->arena + base;
+      h->arena_top = base + total;
+    } else {
+      if (cudaMallocAsync(&extra, std::max<size_t>(total, 256), h->stream) != cudaSuccess) {
+        cudaGetLastError();
+        fail(h, CORUTV_ERR_NOMEM, "device workspace allocation of " + std::to_string(total) + " bytes failed");
+      }
+      mem = static_cast<char*>(extra);
+    }
+    committed = true;
     size_t o = 0;
     for (auto& r : reqs) {
-      *r.first = h->arena + o;
+      *r.first = mem + o;
       o += r.second;
     }
   }
@@ -410,11 +441,41 @@ void cholqr_multi(corutv_handle* h, QrJob* jobs, int njobs, int ell, int64_t ldx
   const int l = ell;
   const int optin = max_optin_smem(h);
   const size_t static_smem = 4096;
-  const size_t aug = 2 * (size_t)l * l * 8;               // [G | I] in shared memory
-  const size_t stage = (size_t)small::NB * (l + small::NB) * 8;  // panel staging (global mode)
+  const size_t aug = 2 * (size_t)l * l * 8;  // [G | I] in one CTA's shared memory
   const bool smem = aug + static_smem <= (size_t)optin;
-  const size_t wbytes = smem ? aug : stage;
-  set_smem(h, small::chol_factor_kernel, wbytes);
+  const size_t cl_smem = (1024 + (size_t)small::NB * (l + small::NB)) * 8;
+  const int cl_cs = l >= 256 ? 16 : 8;
+  if (smem) {
+    set_smem(h, small::chol_factor_kernel, aug);
+  } else {
+    CK(cudaFuncSetAttribute(chc::chol_factor_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)cl_smem));
+    if (cl_cs > 8)
+      CK(cudaFuncSetAttribute(chc::chol_factor_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  }
+  auto launch_factor = [&](QrJob& q, double coeff) {
+    if (smem) {
+      small::chol_factor_kernel<<<1, 512, aug, h->stream>>>(q.w.G, l, ldx, coeff, 1, kKappaPlain, q.w.rinvT,
+                                                          ldx, q.w.gwork, 1, q.w.info);
+      CK_LAUNCH();
+      return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cl_cs, 1, 1);
+    cfg.blockDim = dim3(chc::THREADS, 1, 1);
+    cfg.dynamicSmemBytes = cl_smem;
+    cfg.stream = h->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl_cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, chc::chol_factor_cluster_kernel, (const double*)q.w.G, l, ldx, coeff, 1,
+                          kKappaPlain, q.w.rinvT, ldx, q.w.gwork, q.w.info));
+    ++h->launches;
+  };
   for (int step = 0; step < kMaxQrSteps; ++step) {
     int active = 0;
     for (int j = 0; j < njobs; ++j) {
@@ -424,9 +485,7 @@ void cholqr_multi(corutv_handle* h, QrJob* jobs, int njobs, int ell, int64_t ldx
       const double coeff = 11.0 * (q.rows_global * l + (double)l * (l + 1)) * kUnit;
       run_gemm(h, true, l, l, q.rows, q.cur, ldx, q.cur, ldx, q.w.G, ldx, nullptr, 0, q.w.ws);
       if (q.sharded) allreduce(h, q.w.G, (int64_t)l * ldx);
-      small::chol_factor_kernel<<<1, 512, wbytes, h->stream>>>(
-          q.w.G, l, ldx, coeff, 1, kKappaPlain, q.w.rinvT, ldx, q.w.gwork, smem ? 1 : 0, q.w.info);
-      CK_LAUNCH();
+      launch_factor(q, coeff);
       run_gemm(h, false, q.rows, l, l, q.cur, ldx, q.w.rinvT, ldx, q.nxt, ldx, nullptr, 0, q.w.ws);
       std::swap(q.cur, q.nxt);
       CK(cudaMemcpyAsync(h->pinned + 4 * j, q.w.info, sizeof(small::CholInfo), cudaMemcpyDeviceToHost,
@@ -539,11 +598,105 @@ void jacobi(corutv_handle* h, const double* X, int nv, int len, int64_t ldx, dou
   CK_LAUNCH();
 }
 
+// ------------------------------------------------ Gaussian test matrix
+// np.random.Generator(PCG64(seed)).standard_normal((rows, cols)) on the
+// device (rng.cuh), bit-identical; pcg = {state_hi, state_lo, inc_hi, inc_lo}
+// as expanded by numpy's SeedSequence on the host.  Writes out (ld) and,
+// optionally, the transpose outT (ldT).  One host sync (tail patch).
+void gaussian(corutv_handle* h, const uint64_t* pcg, int64_t rows, int64_t cols, double* out, int64_t ld,
+              double* outT, int64_t ldT) {
+  const int64_t N = rows * cols;
+  if (N <= 0) return;
+  // the wedge path costs ~2.2% extra draws; 1/16 + 4096 leaves a wide margin
+  const int64_t P = N + N / 16 + 4096;
+  const int tail_cap = (int)std::min<int64_t>(P / 128 + 1024, 1 << 26);
+  using MapIt = thrust::transform_iterator<rng::CountToMap, const uint8_t*, uint64_t>;
+  size_t map_bytes = 0, scan_bytes = 0;
+  CK(cub::DeviceScan::ExclusiveScan(nullptr, map_bytes, MapIt(static_cast<const uint8_t*>(nullptr), rng::CountToMap()),
+                                    (uint64_t*)nullptr, rng::ComposeMaps(), rng::kIdentityMap, P));
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int64_t*)nullptr, (int64_t*)nullptr, P));
+  Arena ar(h);
+  double *val, *tail_u;
+  uint8_t *cnt, *tail;
+  uint64_t* prefix;
+  int64_t *starts, *rank, *tail_idx;
+  int *tail_sign, *too_long;
+  unsigned long long* n_tail;
+  void* temp;
+  ar.add(&val, (size_t)P);
+  ar.add(&cnt, (size_t)P);
+  ar.add(&tail, (size_t)P);
+  ar.add(&prefix, (size_t)P);
+  ar.add(&starts, (size_t)P);
+  ar.add(&rank, (size_t)P);
+  ar.add(&tail_idx, (size_t)tail_cap);
+  ar.add(&tail_u, (size_t)tail_cap);
+  ar.add(&tail_sign, (size_t)tail_cap);
+  ar.add(&n_tail, 2);
+  ar.add(&too_long, 4);
+  ar.add((char**)&temp, std::max(map_bytes, scan_bytes) + 256);
+  ar.commit();
+  const int64_t nruns = (P + rng::RUN - 1) / rng::RUN;
+  const int eb = (int)std::min<int64_t>((nruns + 255) / 256, 148 * 32);
+  rng::eval_kernel<<<eb, 256, 0, h->stream>>>(pcg[0], pcg[1], pcg[2], pcg[3], P, val, cnt, tail);
+  CK_LAUNCH();
+  CK(cub::DeviceScan::ExclusiveScan(temp, map_bytes, MapIt(static_cast<const uint8_t*>(cnt), rng::CountToMap()),
+                                    prefix, rng::ComposeMaps(), rng::kIdentityMap, P, h->stream));
+  CK(cudaMemsetAsync(too_long, 0, sizeof(int), h->stream));
+  int nb, tb;
+  launch_grid_1d(P, &nb, &tb);
+  rng::starts_from_maps_kernel<<<nb, tb, 0, h->stream>>>(prefix, cnt, starts, P, too_long);
+  CK_LAUNCH();
+  CK(cub::DeviceScan::ExclusiveSum(temp, scan_bytes, starts, rank, P, h->stream));
+  CK(cudaMemsetAsync(n_tail, 0, sizeof(unsigned long long), h->stream));
+  rng::scatter_kernel<<<nb, tb, 0, h->stream>>>(val, starts, tail, rank, P, N, cols, out, ld, outT, ldT, tail_idx,
+                                                tail_u, tail_sign, n_tail, tail_cap);
+  CK_LAUNCH();
+  // completeness check (samples available) + tail count, one sync
+  CK(cudaMemcpyAsync(h->pinned, rank + (P - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(h->pinned + 1, n_tail, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(h->pinned + 2, starts + (P - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(h->pinned + 3, too_long, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  sync(h);
+  int64_t total = 0, last = 0;
+  unsigned long long ntail = 0;
+  int tl = 0;
+  std::memcpy(&total, h->pinned, 8);
+  std::memcpy(&ntail, h->pinned + 1, 8);
+  std::memcpy(&last, h->pinned + 2, 8);
+  std::memcpy(&tl, h->pinned + 3, 4);
+  if (tl) fail(h, CORUTV_ERR_CUDA, "gaussian: a sample consumed more than 16 draws");
+  if (total + last < N) fail(h, CORUTV_ERR_CUDA, "gaussian: raw stream too short");
+  if (ntail > (unsigned long long)tail_cap) fail(h, CORUTV_ERR_CUDA, "gaussian: tail overflow");
+  if (ntail) {
+    const int nt = (int)ntail;
+    std::vector<int64_t> idx(nt);
+    std::vector<double> u(nt);
+    std::vector<int> sg(nt);
+    CK(cudaMemcpyAsync(idx.data(), tail_idx, nt * 8, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(u.data(), tail_u, nt * 8, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(sg.data(), tail_sign, nt * 4, cudaMemcpyDeviceToHost, h->stream));
+    sync(h);
+    // numpy distributions.c tail: xx = -r^-1 * log1p(-u1); x = +-(r + xx),
+    // with the C library's log1p (the same one numpy calls)
+    volatile double neg_inv_r = -zig::kInvR;
+    for (int t = 0; t < nt; ++t) {
+      const double xx = neg_inv_r * ::log1p(-u[t]);
+      const double x = zig::kR + xx;
+      u[t] = sg[t] ? -x : x;
+    }
+    CK(cudaMemcpyAsync(tail_u, u.data(), nt * 8, cudaMemcpyHostToDevice, h->stream));
+    rng::patch_kernel<<<(nt + 255) / 256, 256, 0, h->stream>>>(tail_idx, tail_u, nt, cols, out, ld, outT, ldT);
+    CK_LAUNCH();
+    sync(h);  // host vectors go out of scope
+  }
+}
+
 // ------------------------------------------------------------ CoR-UTV
 void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, int ell, int q,
-               int variant, const double* omega, double* u, double* t, double* v, int64_t* perm,
-               int64_t* passes_host) {
-  if (!a || !omega || !u || !t || !v) fail(h, CORUTV_ERR_ARG, "null pointer argument");
+               int variant, const double* omega, const uint64_t* pcg, double* u, double* t, double* v,
+               int64_t* perm, int64_t* passes_host) {
+  if (!a || (!omega && !pcg) || !u || !t || !v) fail(h, CORUTV_ERR_ARG, "null pointer argument");
   if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
   if (ell < 1) fail(h, CORUTV_ERR_ARG, "ell must be >= 1, got " + std::to_string(ell));
   if (ell > small::LMAX) fail(h, CORUTV_ERR_ARG, "ell above the supported maximum 640");
@@ -564,7 +717,7 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   const bool a_ok = ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && (lda % 2 == 0);
   const int64_t ldA = a_ok ? lda : round_up(n, 16);
 
-  Arena ar{h};
+  Arena ar(h);
   double *Apad = nullptr, *Xn[2], *XT, *C1a, *C1b, *C2a, *P, *G, *rinvT, *D, *qtT, *B1, *B2t, *pinvB;
   double *G2, *rinvT2, *gwork2, *gwork, *ws, *sigs, *flagd;
   int *flag, *perm32, *jstat;
@@ -609,8 +762,12 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   }
   CK(cudaMemsetAsync(flag, 0, sizeof(int), h->stream));
   // Omega -> Xn[0] (n x ldp) and X^T (l x ldn)
-  copy2d(h, omega, n, l, l, Xn[0], ldp);
-  transpose(h, omega, n, l, l, XT, ldn);
+  if (omega) {
+    copy2d(h, omega, n, l, l, Xn[0], ldp);
+    transpose(h, omega, n, l, l, XT, ldn);
+  } else {
+    gaussian(h, pcg, n, l, Xn[0], ldp, XT, ldn);  // sketch.py:174 on the device
+  }
 
   // power sketch (sketch.py:166-179): C1 = A X ; C2 = A' C1, q+1 times
   int cur = 0;
@@ -732,7 +889,7 @@ void lowrank_op(corutv_handle* h, int mode, const double* u, const double* t, co
   const int J = (int)std::min<int64_t>(8, std::max<int64_t>(1, (cols + 16 * n_tiles - 1) / (16 * n_tiles)));
   const int m_tiles = (int)((rows + gemm::BM - 1) / gemm::BM);
   const int grid = m_tiles * n_tiles;
-  Arena ar{h};
+  Arena ar(h);
   double *Up, *Tr, *Vp, *Wt, *ws, *part, *out;
   long long* cnt;
   ar.add(&Up, (size_t)rows * ldr);
@@ -780,7 +937,7 @@ void lowrank_op(corutv_handle* h, int mode, const double* u, const double* t, co
 
 double sumsq(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda) {
   const int blocks = 148 * 8;
-  Arena ar{h};
+  Arena ar(h);
   double *part, *out;
   ar.add(&part, blocks);
   ar.add(&out, 2);
@@ -801,7 +958,7 @@ void singular_values(corutv_handle* h, const double* a, int64_t m, int64_t n, in
   const int64_t k = std::min(m, n);
   if (k > small::LMAX) fail(h, CORUTV_ERR_ARG, "singular_values: matrix too large for the small-matrix path");
   const int64_t len = std::max(m, n);
-  Arena ar{h};
+  Arena ar(h);
   double *xt = nullptr, *gw;
   int* st;
   if (m >= n) ar.add(&xt, (size_t)n * len);
@@ -830,7 +987,7 @@ void spectral_norm(corutv_handle* h, const double* a, int64_t m, int64_t n, int6
   const double mg = global_rows(h, m);
   if (std::min(mg, (double)n) <= 64) {
     if (sharded) fail(h, CORUTV_ERR_ARG, "spectral_norm: the Jacobi path is single-GPU only");
-    Arena ar{h};
+    Arena ar(h);
     double* sig;
     ar.add(&sig, 128);
     ar.commit();
@@ -851,7 +1008,7 @@ void spectral_norm(corutv_handle* h, const double* a, int64_t m, int64_t n, int6
   const bool a_ok = ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && (lda % 2 == 0);
   const int64_t ldA = a_ok ? lda : round_up(n, 16);
   const int64_t ldb2 = round_up(b, 16);
-  Arena ar{h};
+  Arena ar(h);
   double *Apad = nullptr, *vT, *v, *w, *wT, *z0, *z1, *G, *sig, *ws, *rinvT, *gwork, *G2;
   small::CholInfo* info;
   int* st;
@@ -988,7 +1145,26 @@ int corutv_decompose(corutv_handle* hh, const double* a, int64_t m, int64_t n, i
                      int q_power, int variant, const double* omega, double* u, double* t, double* v,
                      int64_t* perm, int64_t* passes_host) {
   ABI_BEGIN(hh)
-  decompose(h, a, m, n, lda, ell, q_power, variant, omega, u, t, v, perm, passes_host);
+  decompose(h, a, m, n, lda, ell, q_power, variant, omega, nullptr, u, t, v, perm, passes_host);
+  ABI_END
+}
+
+int corutv_decompose_seeded(corutv_handle* hh, const double* a, int64_t m, int64_t n, int64_t lda, int ell,
+                            int q_power, int variant, const uint64_t* pcg_state, double* u, double* t,
+                            double* v, int64_t* perm, int64_t* passes_host) {
+  ABI_BEGIN(hh)
+  if (!pcg_state) fail(h, CORUTV_ERR_ARG, "null pcg_state");
+  uint64_t st[4] = {pcg_state[0], pcg_state[1], pcg_state[2], pcg_state[3]};
+  decompose(h, a, m, n, lda, ell, q_power, variant, nullptr, st, u, t, v, perm, passes_host);
+  ABI_END
+}
+
+int corutv_gaussian(corutv_handle* hh, const uint64_t* pcg_state, int64_t rows, int64_t cols, double* out,
+                    int64_t ld) {
+  ABI_BEGIN(hh)
+  if (!pcg_state || !out || rows < 0 || cols < 0 || ld < cols) fail(h, CORUTV_ERR_ARG, "bad gaussian arguments");
+  uint64_t st[4] = {pcg_state[0], pcg_state[1], pcg_state[2], pcg_state[3]};
+  gaussian(h, st, rows, cols, out, ld, nullptr, 0);
   ABI_END
 }
 
@@ -1003,7 +1179,7 @@ int corutv_gemm(corutv_handle* hh, int trans_a, int64_t M, int64_t N, int64_t K,
   const int64_t arows = trans_a ? K : M, acols = trans_a ? M : K;
   const int64_t ldap = round_up(std::max<int64_t>(acols, 1), 16);
   const int64_t ldbp = round_up(std::max<int64_t>(N, 1), 16);
-  Arena ar{h};
+  Arena ar(h);
   double *bt = nullptr, *ws = nullptr, *ap = nullptr, *bp = nullptr;
   if (!trans_a) ar.add(&bt, (size_t)N * ldbt + 16);
   if (!a_ok) ar.add(&ap, (size_t)arows * ldap + 16);

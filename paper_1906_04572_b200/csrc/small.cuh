@@ -58,6 +58,37 @@ struct CholInfo {
 // panel rows are staged in shared memory (`stage`).
 constexpr int NB = 32;
 
+// One warp factors the nb x nb (nb <= 32) upper block whose columns come
+// from `load(i, k)` (row i, column k, i <= k < nb), keeping column `lane` in
+// registers and broadcasting row j with shuffles (fully unrolled: static
+// register indices).  Out-of-range rows/columns are identity-padded.
+// Returns the factor column in c[] (c[i] = R[i][lane], i <= lane) and a
+// warp-uniform failure flag.
+template <typename Load>
+__device__ __forceinline__ bool warp_chol32(double (&c)[32], int nb, Load load) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    c[i] = (lane < nb && i < nb) ? ((i <= lane) ? load(i, lane) : 0.0) : (i == lane ? 1.0 : 0.0);
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const double d = __shfl_sync(0xffffffffu, c[j], j);
+    bad |= !(d > 0.0) || !isfinite(d);
+    const double r = sqrt(d);
+    double cj = c[j];
+    if (lane > j) cj = cj / r;
+    else if (lane == j) cj = r;
+    c[j] = cj;
+#pragma unroll
+    for (int i = j + 1; i < 32; ++i) {
+      const double rji = __shfl_sync(0xffffffffu, cj, i);
+      if (lane >= i) c[i] = fma(-rji, cj, c[i]);
+    }
+  }
+  return bad;
+}
+
 __device__ __forceinline__ void tile_update(double* W, int ld, const double* P, int pld,
                                             int pcol0, int nb, int i0, int k0, int imax,
                                             int kmax, bool upper, int roff) {
@@ -100,23 +131,12 @@ __device__ bool chol_aug_blocked(double* W, int l, bool wglobal, double* stage, 
     const int nb = min(NB, l - kb);
     // (a) diagonal block, warp 0 (lane = column inside the block)
     if (warp == 0) {
-      int bad = 0;
-      for (int j = 0; j < nb; ++j) {
-        const double d = W[(int64_t)(kb + j) * ld + kb + j];
-        if (!(d > 0.0) || !isfinite(d)) { bad = 1; break; }
-        const double r = sqrt(d);
-        __syncwarp();
-        if (lane > j && lane < nb) W[(int64_t)(kb + j) * ld + kb + lane] /= r;
-        __syncwarp();
-        if (lane == j) W[(int64_t)(kb + j) * ld + kb + j] = r;
-        if (lane > j && lane < nb) {
-          const double f = W[(int64_t)(kb + j) * ld + kb + lane];
-          for (int i = j + 1; i <= lane; ++i)
-            W[(int64_t)(kb + i) * ld + kb + lane] -= W[(int64_t)(kb + j) * ld + kb + i] * f;
-        }
-        __syncwarp();
-      }
-      if (lane == 0) *s_flag = bad;
+      double c[32];
+      const bool bad = warp_chol32(c, nb, [&](int i, int k) { return W[(int64_t)(kb + i) * ld + kb + k]; });
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i <= lane && lane < nb) W[(int64_t)(kb + i) * ld + kb + lane] = c[i];
+      if (lane == 0) *s_flag = bad ? 1 : 0;
     }
     __syncthreads();
     if (*s_flag) return true;
@@ -185,6 +205,36 @@ __device__ bool chol_aug_blocked(double* W, int l, bool wglobal, double* stage, 
   return false;
 }
 
+// Unblocked right-looking Cholesky of [G | I] in shared memory (l <= ~113):
+// two barriers per column, the trailing update spread over warps (rows) and
+// lanes (columns) with no serial chains -- latency-optimal for small cores.
+__device__ bool chol_aug_unblocked(double* W, int l) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = nt >> 5;
+  const int ld = 2 * l;
+  for (int j = 0; j < l; ++j) {
+    const double d = W[j * ld + j];
+    if (!(d > 0.0) || !isfinite(d)) return true;  // uniform
+    const double r = sqrt(d);
+    const int nl = l - j - 1;
+    for (int t = tid; t < nl + j + 1; t += nt) {
+      const int k = (t < nl) ? (j + 1 + t) : (l + (t - nl));
+      W[j * ld + k] = W[j * ld + k] / r;
+    }
+    __syncthreads();
+    if (tid == 0) W[j * ld + j] = r;
+    for (int i = j + 1 + warp; i < l; i += nw) {
+      const double a = W[j * ld + i];
+      double* wi = W + i * ld;
+      const double* wj = W + j * ld;
+      for (int k = i + lane; k < l; k += 32) wi[k] -= a * wj[k];
+      for (int k = lane; k <= j; k += 32) wi[l + k] -= a * wj[l + k];
+    }
+    __syncthreads();
+  }
+  return false;
+}
+
 __device__ double upper_sumsq(const double* W, int l, int ld, int col0, bool lower, double* red) {
   double s = 0.0;
   for (int i = threadIdx.x >> 5; i < l; i += blockDim.x >> 5)
@@ -239,7 +289,7 @@ __global__ void __launch_bounds__(512, 1)
           W[(int64_t)i * ld + k] = g;
         }
       __syncthreads();
-      const bool fail = chol_aug_blocked(W, l, !use_smem, stage, &s_flag);
+      const bool fail = use_smem ? chol_aug_unblocked(W, l) : chol_aug_blocked(W, l, true, stage, &s_flag);
       __syncthreads();
       if (fail) {
         if (!shifted) { shifted = 1; continue; }

@@ -23,7 +23,7 @@ import numpy as np
 
 from . import _device as dev
 from . import _lib
-from .sketch import _VARIANT_CODE, CorUtvFactors, PassCounter, SketchConfig, gaussian_matrix
+from .sketch import _VARIANT_CODE, CorUtvFactors, PassCounter, SketchConfig, pcg_state
 
 __all__ = ["row_range", "RowShardComm", "corutv_sharded"]
 
@@ -99,10 +99,10 @@ def corutv_sharded(a_local, cfg: SketchConfig, comm: RowShardComm, counter: Pass
     A, was_host = dev.to_device(a_local, "a")
     m_loc, n = A.shape
     ell = cfg.ell
-    if omega is None:
-        omega = gaussian_matrix(n, ell, cfg.seed)  # identical on every rank
-    om = (omega if dev.is_device_tensor(omega) else torch.from_numpy(np.ascontiguousarray(omega)))
-    om = om.to(A.device, torch.float64).contiguous()
+    om = None
+    if omega is not None:
+        om = (omega if dev.is_device_tensor(omega) else torch.from_numpy(np.ascontiguousarray(omega)))
+        om = om.to(A.device, torch.float64).contiguous()
     u = torch.empty((m_loc, ell), dtype=torch.float64, device=A.device)
     t = torch.empty((ell, ell), dtype=torch.float64, device=A.device)
     v = torch.empty((n, ell), dtype=torch.float64, device=A.device)
@@ -111,9 +111,14 @@ def corutv_sharded(a_local, cfg: SketchConfig, comm: RowShardComm, counter: Pass
     h = _lib.handle(A.device.index)
     comm.attach(h)
     try:
-        h.call("corutv_decompose", dev.ptr(A), m_loc, n, A.stride(0), ell, cfg.q_power,
-               _VARIANT_CODE[cfg.variant], dev.ptr(om), dev.ptr(u), dev.ptr(t), dev.ptr(v),
-               dev.ptr(perm), ctypes.byref(passes))
+        if om is None:  # every rank draws the identical Omega on its device
+            h.call("corutv_decompose_seeded", dev.ptr(A), m_loc, n, A.stride(0), ell, cfg.q_power,
+                   _VARIANT_CODE[cfg.variant], pcg_state(cfg.seed), dev.ptr(u), dev.ptr(t),
+                   dev.ptr(v), dev.ptr(perm), ctypes.byref(passes))
+        else:
+            h.call("corutv_decompose", dev.ptr(A), m_loc, n, A.stride(0), ell, cfg.q_power,
+                   _VARIANT_CODE[cfg.variant], dev.ptr(om), dev.ptr(u), dev.ptr(t), dev.ptr(v),
+                   dev.ptr(perm), ctypes.byref(passes))
     finally:
         comm.detach(h)
     if counter is not None:

@@ -25,7 +25,7 @@ from . import _device as dev
 from . import _lib
 from .dense import singular_values, spectral_norm
 from .errors import ConvergenceError
-from .sketch import SketchConfig, corutv, gaussian_matrix
+from .sketch import SketchConfig, corutv
 
 __all__ = [
     "AlmConfig",
@@ -172,7 +172,7 @@ def alm_corutv(m, cfg: AlmConfig) -> RpcaSolution:
     nnz = ctypes.c_int64(0)
     for j in range(cfg.max_iter):
         scfg = SketchConfig(ell=cap, q_power=cfg.q_power, seed=(cfg.seed + j) % 2 ** 64)
-        f = corutv(src, scfg, omega=gaussian_matrix(w_, cap, scfg.seed))
+        f = corutv(src, scfg)  # Omega = gaussian_matrix(w, cap, seed + j), drawn on the device
         rank = _truncate(f, 1.0 / mu)
         caps.append(cap)
         cap = _next_cap(cap, rank, limit, grow)

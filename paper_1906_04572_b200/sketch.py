@@ -117,6 +117,30 @@ class PassCounter:
         self.passes += n
 
 
+def pcg_state(seed: int):
+    """numpy's PCG64(seed) starting state as {state_hi, state_lo, inc_hi,
+    inc_lo} (SeedSequence expansion on the host; the draws themselves are
+    generated on the device, bit-identical to gaussian_matrix)."""
+    st = np.random.PCG64(seed).state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    m64 = (1 << 64) - 1
+    return (ctypes.c_uint64 * 4)(s >> 64, s & m64, inc >> 64, inc & m64)
+
+
+def gaussian_matrix_device(rows: int, cols: int, seed: int, device=None):
+    """gaussian_matrix(rows, cols, seed) generated on the B200 (PCG64 +
+    ziggurat, bit-identical to numpy)."""
+    torch = dev.torch_mod()
+    if rows < 1 or cols < 1:
+        raise ValueError(f"gaussian_matrix needs positive dims, got {rows}x{cols}")
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    out = torch.empty((rows, cols), dtype=torch.float64, device=device)
+    h = _lib.handle(out.device.index)
+    h.call("corutv_gaussian", pcg_state(seed), rows, cols, dev.ptr(out), cols)
+    return out
+
+
 def _omega_device(omega, n, ell, seed, device_like):
     torch = dev.torch_mod()
     if omega is None:
@@ -148,16 +172,22 @@ def corutv(a, cfg: SketchConfig, counter: PassCounter | None = None, omega=None)
         cfg.validated_for(m, n)
     A, was_host = dev.to_device(a, "a")
     ell = cfg.ell
-    om = _omega_device(omega, n, ell, cfg.seed, A)
     u = torch.empty((m, ell), dtype=torch.float64, device=A.device)
     t = torch.empty((ell, ell), dtype=torch.float64, device=A.device)
     v = torch.empty((n, ell), dtype=torch.float64, device=A.device)
     perm = torch.empty((ell,), dtype=torch.int64, device=A.device)
     passes = ctypes.c_int64(0)
     h = _lib.handle(A.device.index)
-    h.call("corutv_decompose", dev.ptr(A), m, n, A.stride(0), ell, cfg.q_power,
-           _VARIANT_CODE[cfg.variant], dev.ptr(om), dev.ptr(u), dev.ptr(t), dev.ptr(v),
-           dev.ptr(perm), ctypes.byref(passes))
+    if omega is None:
+        # Omega = gaussian_matrix(n, ell, seed) drawn on the device (sketch.py:174)
+        h.call("corutv_decompose_seeded", dev.ptr(A), m, n, A.stride(0), ell, cfg.q_power,
+               _VARIANT_CODE[cfg.variant], pcg_state(cfg.seed), dev.ptr(u), dev.ptr(t),
+               dev.ptr(v), dev.ptr(perm), ctypes.byref(passes))
+    else:
+        om = _omega_device(omega, n, ell, cfg.seed, A)
+        h.call("corutv_decompose", dev.ptr(A), m, n, A.stride(0), ell, cfg.q_power,
+               _VARIANT_CODE[cfg.variant], dev.ptr(om), dev.ptr(u), dev.ptr(t), dev.ptr(v),
+               dev.ptr(perm), ctypes.byref(passes))
     if counter is not None:
         counter.add(passes.value)
     return CorUtvFactors(u=dev.to_output(u, was_host), t=dev.to_output(t, was_host),

@@ -369,3 +369,27 @@ def test_alm_c4_shaped_reduced():
     assert np.linalg.norm(sol.l - ref["l"]) <= 1e-8 * np.linalg.norm(ref["l"])
     assert np.linalg.norm(sol.s - ref["s"]) <= 1e-8 * np.linalg.norm(ref["s"])
     assert abs(P.spectral_norm(m) - 1.25 / mu0) <= 1e-12 * (1.25 / mu0)
+
+
+# ------------------------------------------------------- device Omega
+@pytest.mark.parametrize("seed,rows,cols", [(0, 30, 7), (12345, 1000, 15), (7, 3000, 50),
+                                            (2**63 + 5, 4096, 110), (99, 10000, 51)])
+def test_device_gaussian_is_numpy_bitwise(seed, rows, cols):
+    """sketch.py:63-68 on the device: PCG64 + ziggurat, bit-identical."""
+    dev_om = P.sketch.gaussian_matrix_device(rows, cols, seed).cpu().numpy()
+    assert np.array_equal(dev_om, P.gaussian_matrix(rows, cols, seed))
+
+
+def test_device_gaussian_large_covers_tail_path():
+    # ~2.6e-4 of samples take the tail path (host-finished with libm log1p)
+    om = P.sketch.gaussian_matrix_device(20000, 110, 4242).cpu().numpy()
+    ref = P.gaussian_matrix(20000, 110, 4242)
+    assert np.array_equal(om, ref)
+    assert np.abs(ref).max() > 3.6541528853610088  # tail samples present
+
+
+def test_seeded_and_explicit_omega_paths_agree(golden):
+    a = golden["cu_noisy_q1"]["a"]
+    f1 = P.corutv(a, P.SketchConfig(ell=16, q_power=1, seed=9))
+    f2 = P.corutv(a, P.SketchConfig(ell=16, q_power=1), omega=P.gaussian_matrix(a.shape[1], 16, 9))
+    assert np.array_equal(f1.t, f2.t) and np.array_equal(f1.u, f2.u)

@@ -1,4 +1,2 @@
-python tools/small_sweep.py 600 > gpurun_out/sw_600.log 2>&1 && ncu --set full --import-source on --clock-control none -k regex:qrcp_cluster -c 1 -o gpurun_out/prof_qrcp600 python tools/small_sweep.py 600 > gpurun_out/ncu_q600.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:chol_factor -c 1 -o gpurun_out/prof_chol600 python tools/small_sweep.py 600 > gpurun_out/ncu_c600.log 2>&1
-python tools/small_sweep.py 110 > gpurun_out/sw_110.log 2>&1 && ncu --set full --import-source on --clock-control none -k regex:chol_factor -c 1 -o gpurun_out/prof_chol110 python tools/small_sweep.py 110 > gpurun_out/ncu_c110.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:qrcp_cluster -c 1 -o gpurun_out/prof_qrcp110 python tools/small_sweep.py 110 > gpurun_out/ncu_q110.log 2>&1
+python tools/c4_iter0.py > gpurun_out/c4_iter0.log 2>&1
+python tools/c4_parity.py > gpurun_out/c4_parity.log 2>&1
