@@ -530,21 +530,15 @@ double* cholqr(corutv_handle* h, double* xa, double* xb, int64_t rows, int ell, 
 void qrcp(corutv_handle* h, const double* D, int l, int64_t ldd, double* T, int64_t ldt, double* qtT,
           int64_t ldq, long long* perm_out, int* perm32, double* gwork) {
   const int optin = max_optin_smem(h);
-  if (l <= 32) {
-    const size_t stat = 5 * small::LMAX * 8 + 4 * small::LMAX * 4 + 1024;
-    const size_t one = (size_t)l * l * 8;
-    int smR = 0, smQ = 0;
-    size_t dyn = 0;
-    if (2 * one + stat <= (size_t)optin) {
-      smR = smQ = 1;
-      dyn = 2 * one;
-    } else if (one + stat <= (size_t)optin) {
-      smR = 1;
-      dyn = one;
-    }
-    if (dyn) set_smem(h, small::qrcp_kernel, dyn);
-    small::qrcp_kernel<<<1, 1024, dyn, h->stream>>>(D, l, ldd, T, ldt, qtT, ldq, perm_out, perm32, gwork,
-                                                     smR, smQ);
+  // small cores: one CTA with R and Q in shared memory, ~G*l threads
+  const size_t one = (size_t)l * l * 8;
+  const size_t stat128 = 5 * 128 * 8 + 4 * 128 * 4 + 1024;
+  if (l <= 128 && 2 * one + stat128 <= (size_t)optin) {
+    const int G = l <= 64 ? 4 : 2;
+    const int threads = (int)std::min<int64_t>(1024, round_up((int64_t)l * G, 32));
+    auto kern = (G == 4) ? small::qrcp_kernel<128, 4> : small::qrcp_kernel<128, 2>;
+    set_smem(h, kern, 2 * one);
+    kern<<<1, threads, 2 * one, h->stream>>>(D, l, ldd, T, ldt, qtT, ldq, perm_out, perm32, gwork, 1, 1);
     CK_LAUNCH();
     return;
   }
@@ -553,7 +547,7 @@ void qrcp(corutv_handle* h, const double* D, int l, int64_t ldd, double* T, int6
   int cs = 2;
   for (; cs <= 16; cs *= 2) {
     const int cw = (l + cs - 1) / cs;
-    if ((size_t)cw * l * 8 * 2 + stat <= (size_t)optin) break;  // R and Q on chip
+    if (cw <= qc::MAXCW && (size_t)cw * l * 8 * 2 + stat <= (size_t)optin) break;  // R and Q on chip
   }
   bool q_smem = true;
   if (cs > 16) {
@@ -562,7 +556,8 @@ void qrcp(corutv_handle* h, const double* D, int l, int64_t ldd, double* T, int6
   }
   const int cw = (l + cs - 1) / cs;
   const size_t dyn = (size_t)cw * l * 8 * (q_smem ? 2 : 1);
-  if (dyn + stat > (size_t)optin) fail(h, CORUTV_ERR_ARG, "QRCP core too large for a 16-CTA cluster");
+  if (cw > qc::MAXCW || dyn + stat > (size_t)optin)
+    fail(h, CORUTV_ERR_ARG, "QRCP core too large for a 16-CTA cluster");
   CK(cudaFuncSetAttribute(qc::qrcp_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
   if (cs > 8) CK(cudaFuncSetAttribute(qc::qrcp_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};

@@ -315,41 +315,95 @@ __global__ void __launch_bounds__(THREADS, 1)
   bool bad = false;
   mainloop<J, false, false>(sm, &mapU, &mapW, m0, n0, 0, t.k_tiles, acc, wm, wn, lane, nvf, mvf, bad);
 
+  // Stage the 128 x 16J tile of L in shared memory (the pipeline buffers are
+  // free now), then stream it row by row: each warp owns rows, lanes cover
+  // 2 consecutive columns (double2), so every global access of M, Y, S, G is
+  // a fully used 512-byte warp transaction; 4 rows in flight per warp.
+  __syncthreads();
+  constexpr int TN = 16 * J;        // tile columns
+  constexpr int LDT = TN + 2;       // padded row (doubles), keeps double2 alignment
+  double* tileL = sm.a;             // 128 x LDT doubles (<= 130 KB)
   const int r8 = lane >> 2, c4 = lane & 3;
-  double ssum = 0.0;
-  long long cnt = 0;
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi) {
-    const int row = m0 + wm * 32 + mi * 8 + r8;
-    if (row >= t.M) continue;
+    const int row = wm * 32 + mi * 8 + r8;
 #pragma unroll
     for (int nj = 0; nj < J; ++nj) {
-      const int col = ncol0 + nj * 8 + 2 * c4;
+      const int col = wn * 8 * J + nj * 8 + 2 * c4;
+      *reinterpret_cast<double2*>(tileL + row * LDT + col) = make_double2(acc.v[mi][nj][0], acc.v[mi][nj][1]);
+    }
+  }
+  __syncthreads();
+  double ssum = 0.0;
+  long long cnt = 0;
+  const int ncols = min(TN, t.N - n0);
+  const bool vec = ((p.ld & 1) == 0);
+  for (int rb = warp * 4; rb < BM; rb += NCW * 4) {
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        if (col + e >= t.N) continue;
-        const int64_t idx = (int64_t)row * p.ld + col + e;
-        const double l = acc.v[mi][nj][e];
+    for (int rr = 0; rr < 4; ++rr) {
+      const int row = rb + rr;
+      const int grow = m0 + row;
+      if (grow >= t.M) continue;
+      for (int c = 2 * lane; c < ncols; c += 64) {
+        const int64_t idx = (int64_t)grow * p.ld + n0 + c;
+        const double2 l2 = *reinterpret_cast<const double2*>(tileL + row * LDT + c);
+        const bool pair = vec && (c + 1 < ncols);
+        double lv[2] = {l2.x, l2.y};
+        double mv[2] = {0.0, 0.0}, yv[2] = {0.0, 0.0};
+        if (MODE != LR_STORE) {
+          if (pair) {
+            const double2 m2 = *reinterpret_cast<const double2*>(p.m_mat + idx);
+            mv[0] = m2.x; mv[1] = m2.y;
+            if (MODE == LR_ALM) {
+              const double2 y2 = *reinterpret_cast<const double2*>(p.y + idx);
+              yv[0] = y2.x; yv[1] = y2.y;
+            }
+          } else {
+            mv[0] = p.m_mat[idx];
+            if (c + 1 < ncols) mv[1] = p.m_mat[idx + 1];
+            if (MODE == LR_ALM) {
+              yv[0] = p.y[idx];
+              if (c + 1 < ncols) yv[1] = p.y[idx + 1];
+            }
+          }
+        }
+        double sv[2], yn[2], gv[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (e == 1 && c + 1 >= ncols) continue;
+          const double l = lv[e];
+          if (MODE == LR_RESID) {
+            const double d = mv[e] - l;
+            ssum = fma(d, d, ssum);
+          } else if (MODE == LR_ALM) {
+            // rpca.py:211-214, operation order mirrored from the numpy source
+            const double mm = mv[e], yy = yv[e];
+            const double g = (mm - l) + yy / p.mu;
+            const double ag = fabs(g) - p.lam_over_mu;
+            const double sg = (g > 0.0) ? 1.0 : ((g < 0.0) ? -1.0 : g);
+            sv[e] = sg * fmax(ag, 0.0);
+            const double z = (mm - l) - sv[e];
+            yn[e] = yy + p.mu * z;
+            gv[e] = (mm - sv[e]) + yn[e] / p.mu_next;
+            ssum = fma(z, z, ssum);
+            cnt += (fabs(sv[e]) > 1e-12) ? 1 : 0;
+          }
+        }
         if (MODE == LR_STORE) {
-          p.g_next[idx] = l;
-        } else if (MODE == LR_RESID) {
-          const double d = p.m_mat[idx] - l;
-          ssum = fma(d, d, ssum);
-        } else {
-          // rpca.py:211-214, operation order mirrored from the numpy source
-          const double mm = p.m_mat[idx];
-          const double yy = p.y[idx];
-          const double g = (mm - l) + yy / p.mu;
-          const double ag = fabs(g) - p.lam_over_mu;
-          const double sg = (g > 0.0) ? 1.0 : ((g < 0.0) ? -1.0 : g);
-          const double sv = sg * fmax(ag, 0.0);
-          const double z = (mm - l) - sv;
-          const double yn = yy + p.mu * z;
-          p.s[idx] = sv;
-          p.y[idx] = yn;
-          p.g_next[idx] = (mm - sv) + yn / p.mu_next;
-          ssum = fma(z, z, ssum);
-          cnt += (fabs(sv) > 1e-12) ? 1 : 0;
+          if (pair) *reinterpret_cast<double2*>(p.g_next + idx) = make_double2(lv[0], lv[1]);
+          else {
+            p.g_next[idx] = lv[0];
+            if (c + 1 < ncols) p.g_next[idx + 1] = lv[1];
+          }
+        } else if (MODE == LR_ALM) {
+          if (pair) {
+            *reinterpret_cast<double2*>(p.s + idx) = make_double2(sv[0], sv[1]);
+            *reinterpret_cast<double2*>(p.y + idx) = make_double2(yn[0], yn[1]);
+            *reinterpret_cast<double2*>(p.g_next + idx) = make_double2(gv[0], gv[1]);
+          } else {
+            p.s[idx] = sv[0]; p.y[idx] = yn[0]; p.g_next[idx] = gv[0];
+            if (c + 1 < ncols) { p.s[idx + 1] = sv[1]; p.y[idx + 1] = yn[1]; p.g_next[idx + 1] = gv[1]; }
+          }
         }
       }
     }

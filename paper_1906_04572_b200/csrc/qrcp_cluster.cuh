@@ -31,10 +31,11 @@ namespace cg = cooperative_groups;
 constexpr int THREADS = 1024;
 constexpr int NW = THREADS / 32;
 constexpr int LMAX = 640;
+constexpr int MAXCW = 64;  // columns owned per CTA (host picks CS accordingly)
 
 struct Shared {
-  double nrm[48], ref[48];
-  int done[48];
+  double nrm[MAXCW], ref[MAXCW];
+  int done[MAXCW];
   double cand_v[2][16];
   int cand_q[2][16];
   int l2p[2][LMAX];

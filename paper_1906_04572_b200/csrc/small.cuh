@@ -336,9 +336,9 @@ __device__ __forceinline__ double group_sum(double v) {
   return v;
 }
 
-template <int G>
+template <int G, int LM>
 __device__ void qrcp_body(double* R, double* Q, int l, double* nrm, double* ref, double* tau,
-                          double* vhead, double* diag, int (*l2p)[LMAX], int* done, int* has_ref,
+                          double* vhead, double* diag, int (*l2p)[LM], int* done, int* has_ref,
                           const int** fin_out) {
   const int lane = threadIdx.x & 31;
   const int nt = blockDim.x;
@@ -445,19 +445,23 @@ __device__ void qrcp_body(double* R, double* Q, int l, double* nrm, double* ref,
   }
 }
 
-__global__ void __launch_bounds__(THREADS, 1)
+// LM: capacity of the per-column arrays (the core must satisfy l <= LM);
+// G: lanes per column.  The host launches ~G * l threads so the redundant
+// per-warp pivot/norm work stays small (few warps) for small cores.
+template <int LM, int G>
+__global__ void __launch_bounds__(1024, 1)
     qrcp_kernel(const double* __restrict__ D, int l, int64_t ldd, double* __restrict__ T,
                 int64_t ldt, double* __restrict__ qtT, int64_t ldq, long long* perm_out,
                 int* perm32, double* gwork, int smem_R, int smem_Q) {
   extern __shared__ double dsm[];
-  __shared__ double nrm[LMAX];
-  __shared__ double ref[LMAX];
-  __shared__ double tau[LMAX];
-  __shared__ double vhead[LMAX];
-  __shared__ double diag[LMAX];
-  __shared__ int l2p[2][LMAX];
-  __shared__ int done[LMAX];
-  __shared__ int has_ref[LMAX];
+  __shared__ double nrm[LM];
+  __shared__ double ref[LM];
+  __shared__ double tau[LM];
+  __shared__ double vhead[LM];
+  __shared__ double diag[LM];
+  __shared__ int l2p[2][LM];
+  __shared__ int done[LM];
+  __shared__ int has_ref[LM];
   const int lane = threadIdx.x & 31;
   const int nt = blockDim.x;
   double* R = smem_R ? dsm : gwork;
@@ -480,13 +484,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   __syncthreads();
   const int* fin = nullptr;
-  const int per = nt / l;  // lanes available per column
-  if (per >= 32) qrcp_body<32>(R, Q, l, nrm, ref, tau, vhead, diag, l2p, done, has_ref, &fin);
-  else if (per >= 16) qrcp_body<16>(R, Q, l, nrm, ref, tau, vhead, diag, l2p, done, has_ref, &fin);
-  else if (per >= 8) qrcp_body<8>(R, Q, l, nrm, ref, tau, vhead, diag, l2p, done, has_ref, &fin);
-  else if (per >= 4) qrcp_body<4>(R, Q, l, nrm, ref, tau, vhead, diag, l2p, done, has_ref, &fin);
-  else if (per >= 2) qrcp_body<2>(R, Q, l, nrm, ref, tau, vhead, diag, l2p, done, has_ref, &fin);
-  else qrcp_body<4>(R, Q, l, nrm, ref, tau, vhead, diag, l2p, done, has_ref, &fin);
+  qrcp_body<G, LM>(R, Q, l, nrm, ref, tau, vhead, diag, l2p, done, has_ref, &fin);
   __syncthreads();
   for (int i = threadIdx.x >> 5; i < l; i += nt >> 5)
     for (int c = lane; c < l; c += 32) {

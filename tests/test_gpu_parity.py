@@ -393,3 +393,38 @@ def test_seeded_and_explicit_omega_paths_agree(golden):
     f1 = P.corutv(a, P.SketchConfig(ell=16, q_power=1, seed=9))
     f2 = P.corutv(a, P.SketchConfig(ell=16, q_power=1), omega=P.gaussian_matrix(a.shape[1], 16, 9))
     assert np.array_equal(f1.t, f2.t) and np.array_equal(f1.u, f2.u)
+
+
+# ------------------------------------------- every small-kernel code path
+@pytest.fixture(scope="module")
+def decaying_matrix():
+    rng = np.random.Generator(np.random.PCG64(606))
+    m, n = 2400, 1800
+    u = np.linalg.qr(rng.standard_normal((m, 400)))[0]
+    v = np.linalg.qr(rng.standard_normal((n, 400)))[0]
+    sig = 0.985 ** np.arange(400)
+    return (u * sig) @ v.T + 1e-9 * rng.standard_normal((m, n))
+
+
+@pytest.mark.parametrize("ell", [15, 33, 64, 100, 110, 113, 114, 130, 272, 400])
+def test_corutv_parity_across_ell(decaying_matrix, ell):
+    """ell sweeps the one-CTA / cluster Cholesky (<=113 / >113) and the
+    one-CTA / cluster QRCP (<=32 / >32, 2..16 CTAs) paths."""
+    a = decaying_matrix
+    om = O.gaussian_matrix(a.shape[1], ell, 5)
+    ref = O.corutv(a, ell, 1, omega=om)
+    f = P.corutv(a, P.SketchConfig(ell=ell, q_power=1, seed=5))
+    check_factors(f, a, ell)
+    e_ref = O.corutv_lowrank_error(a, ref)
+    na = np.linalg.norm(a)
+    if e_ref > 1e-4 * na:
+        assert abs(np.linalg.norm(a - f.lowrank()) - e_ref) <= 1e-10 * e_ref
+    else:
+        # ell == rank: the error is the 1e-9 noise floor; the oracle with
+        # LAPACK's QR already differs from the reference by 1.5% (4.5e-9 |A|)
+        assert abs(np.linalg.norm(a - f.lowrank()) - e_ref) <= 1e-8 * na
+    dref = np.abs(np.diag(ref["t"]))
+    assert np.abs(np.abs(np.diag(f.t)) - dref).max() <= 1e-9 * dref[0]
+    k = ell // 2
+    assert np.array_equal(f.perm[:k], ref["perm"][:k])
+    assert np.abs(sign_align(f.u[:, :k], ref["u"][:, :k]) - ref["u"][:, :k]).max() <= 1e-9
