@@ -60,6 +60,16 @@ CU_DEV void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, i
       : "memory");
 }
 
+// 3-D tiled load: box at (c0, c1, c2).
+CU_DEV void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0, int32_t c1,
+                        int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 // ---------------------------------------------------------------- FP64 MMA
 // D(8x8) += A(8x4, row) * B(4x8, col).  Lane l holds A[l>>2][l&3],
 // B[l&3][l>>2], and C[l>>2][2*(l&3) + {0,1}].  SASS: DMMA.884.

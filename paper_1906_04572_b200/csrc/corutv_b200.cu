@@ -217,6 +217,23 @@ CUtensorMap make_map(corutv_handle* h, const double* base, int64_t inner, int64_
   return m;
 }
 
+// 3-D view of a row-major M-major operand: dims {16 columns, rows, column
+// groups}, strides {ld, 16 doubles}; box {16, BK, groups}.  Valid when the
+// last column group stays inside every row (cols % 16 == 0 or padded ld).
+bool make_map3d(corutv_handle* h, const double* base, int64_t cols, int64_t rows, int64_t ld, int groups,
+                CUtensorMap* m) {
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld & 1)) return false;
+  if (cols % 16 != 0 && ld < round_up(cols, 16)) return false;
+  cuuint64_t dims[3] = {16, (cuuint64_t)std::max<int64_t>(rows, 1), (cuuint64_t)((cols + 15) / 16)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 8), 128};
+  cuuint32_t box[3] = {16, (cuuint32_t)gemm::BK, (cuuint32_t)groups};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn(h)(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // ------------------------------------------------------------------- GEMM
 struct GemmPlan {
   int J, n_tiles, m_tiles, k_tiles, splits, kps;
@@ -322,9 +339,12 @@ void run_gemm(corutv_handle* h, bool mm, int64_t M, int64_t N, int64_t K, const 
   t.k_tiles_per_split = p.kps;
   t.splits = p.splits;
   CUtensorMap ma, mb;
+  t.mm3d = 0;
   if (!mm) {
     ma = make_map(h, A, K, M, lda, gemm::BM);
     mb = make_map(h, B, K, N, ldb, 16 * p.J);
+  } else if (make_map3d(h, A, M, K, lda, gemm::BM / 16, &ma) && make_map3d(h, B, N, K, ldb, p.J, &mb)) {
+    t.mm3d = 1;
   } else {
     ma = make_map(h, A, M, K, lda, gemm::BK);
     mb = make_map(h, B, N, K, ldb, gemm::BK);
@@ -850,11 +870,11 @@ void launch_lr_t(corutv_handle* h, const CUtensorMap& mu, const CUtensorMap& mw,
   auto kern = gemm::lowrank_kernel<J, MODE>;
   static bool configured = false;
   if (!configured) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::smem_bytes(J)));
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::lr_smem_bytes(J)));
     configured = true;
   }
   ProfScope ps(h, 3, 2.0 * t.M * t.N * (double)t.K);
-  kern<<<grid, gemm::THREADS, gemm::smem_bytes(J), h->stream>>>(mu, mw, t, p);
+  kern<<<grid, gemm::THREADS, gemm::lr_smem_bytes(J), h->stream>>>(mu, mw, t, p);
   CK_LAUNCH();
 }
 
@@ -865,11 +885,7 @@ void launch_lr(corutv_handle* h, int J, const CUtensorMap& mu, const CUtensorMap
     case 1: launch_lr_t<1, MODE>(h, mu, mw, t, p, grid); break;
     case 2: launch_lr_t<2, MODE>(h, mu, mw, t, p, grid); break;
     case 3: launch_lr_t<3, MODE>(h, mu, mw, t, p, grid); break;
-    case 4: launch_lr_t<4, MODE>(h, mu, mw, t, p, grid); break;
-    case 5: launch_lr_t<5, MODE>(h, mu, mw, t, p, grid); break;
-    case 6: launch_lr_t<6, MODE>(h, mu, mw, t, p, grid); break;
-    case 7: launch_lr_t<7, MODE>(h, mu, mw, t, p, grid); break;
-    default: launch_lr_t<8, MODE>(h, mu, mw, t, p, grid); break;
+    default: launch_lr_t<4, MODE>(h, mu, mw, t, p, grid); break;
   }
 }
 
@@ -880,8 +896,10 @@ void lowrank_op(corutv_handle* h, int mode, const double* u, const double* t, co
                 int64_t rows, int64_t cols, int ell, int r, gemm::LrParams p, double out2[2]) {
   if (rows < 1 || cols < 1 || ell < 1 || r < 0 || r > ell) fail(h, CORUTV_ERR_ARG, "bad low-rank operand shape");
   const int64_t ldr = round_up(std::max(r, 1), 16), ldl = round_up(ell, 16);
-  const int n_tiles = (int)((cols + 127) / 128);
-  const int J = (int)std::min<int64_t>(8, std::max<int64_t>(1, (cols + 16 * n_tiles - 1) / (16 * n_tiles)));
+  // 128 x 64 tiles (J <= 4): small shared/register footprint -> 2-3 CTAs per
+  // SM, so one CTA's TMA mainloop overlaps another's memory-bound epilogue
+  const int n_tiles = (int)((cols + 63) / 64);
+  const int J = (int)std::min<int64_t>(4, std::max<int64_t>(1, (cols + 16 * n_tiles - 1) / (16 * n_tiles)));
   const int m_tiles = (int)((rows + gemm::BM - 1) / gemm::BM);
   const int grid = m_tiles * n_tiles;
   Arena ar(h);
@@ -897,6 +915,7 @@ void lowrank_op(corutv_handle* h, int mode, const double* u, const double* t, co
   ar.add(&out, 2);
   ar.commit();
   gemm::Tile tl;
+  tl.mm3d = 0;
   tl.M = (int)rows;
   tl.N = (int)cols;
   tl.K = r;

@@ -36,6 +36,14 @@ __host__ __device__ constexpr int num_stages(int J) {
 __host__ __device__ constexpr int smem_bytes(int J) {
   return 1024 /*align slack*/ + num_stages(J) * stage_bytes(J) + 2 * 8 * 8 + 64;
 }
+// low-rank (ALM / residual / store) kernels: K = r is short, so 2 stages; the
+// same bytes are reused to stage the 128 x (16J + 2) result tile.
+constexpr int LR_STAGES = 2;
+__host__ __device__ constexpr int lr_tile_bytes(int J) { return BM * (16 * J + 2) * 8; }
+__host__ __device__ constexpr int lr_data_bytes(int J) {
+  return LR_STAGES * stage_bytes(J) > lr_tile_bytes(J) ? LR_STAGES * stage_bytes(J) : lr_tile_bytes(J);
+}
+__host__ __device__ constexpr int lr_smem_bytes(int J) { return 1024 + lr_data_bytes(J) + 2 * 8 * 8 + 64; }
 
 struct Tile {
   int M, N, K;          // problem (this launch)
@@ -43,6 +51,7 @@ struct Tile {
   int k_tiles;          // total k tiles (ceil(K / 16))
   int k_tiles_per_split;
   int splits;
+  int mm3d;             // MM operands: one 3-D box per stage instead of 2-D boxes
 };
 
 // Accumulator for one consumer warp: 4 (M) x J (N) DMMA fragments.
@@ -66,15 +75,14 @@ struct Smem {
 
 // Pointer arithmetic on the __shared__ array (never through an integer) so
 // the compiler keeps the shared address space and emits LDS.
-template <int J>
+template <int J, int S, int DATA = S * (a_stage_bytes() + b_stage_bytes(J))>
 __device__ __forceinline__ Smem carve(unsigned char* raw) {
   const uint32_t pad = (1024u - (smem_u32(raw) & 1023u)) & 1023u;
   unsigned char* p = raw + pad;
-  constexpr int S = num_stages(J);
   Smem s;
   s.a = reinterpret_cast<double*>(p);
   s.b = reinterpret_cast<double*>(p + S * a_stage_bytes());
-  s.full = reinterpret_cast<uint64_t*>(p + S * (a_stage_bytes() + b_stage_bytes(J)));
+  s.full = reinterpret_cast<uint64_t*>(p + DATA);
   s.empty = s.full + 8;
   return s;
 }
@@ -83,13 +91,17 @@ __device__ __forceinline__ Smem carve(unsigned char* raw) {
 template <int J, bool MM>
 __device__ __forceinline__ void issue_stage(const Smem& sm, const CUtensorMap* mapA,
                                             const CUtensorMap* mapB, int m0, int n0, int kt,
-                                            int st) {
+                                            int st, int mm3d = 0) {
   mbar_arrive_expect_tx(&sm.full[st], stage_bytes(J));
   double* sa = sm.a + st * (BM * BK);
   double* sb = sm.b + st * (16 * J * BK);
   if (!MM) {
     tma_load_2d(sa, mapA, &sm.full[st], kt * BK, m0);
     tma_load_2d(sb, mapB, &sm.full[st], kt * BK, n0);
+  } else if (mm3d) {
+    // dims {16 cols, rows, column groups}: the box lands as [group][row][16]
+    tma_load_3d(sa, mapA, &sm.full[st], 0, kt * BK, m0 / 16);
+    tma_load_3d(sb, mapB, &sm.full[st], 0, kt * BK, n0 / 16);
   } else {
 #pragma unroll
     for (int bx = 0; bx < BM / 16; ++bx)
@@ -115,12 +127,11 @@ __device__ __forceinline__ void issue_stage(const Smem& sm, const CUtensorMap* m
 // MM: both operands M-major (16-column boxes, rows = k); lanes read rows
 //     k = s + 4(lane&3): the 4 rows of a fragment fall on two different
 //     (k & 7) swizzle phases, 2 wavefronts per 256 B, the minimum.
-template <int J, bool MM, bool CHECK>
+template <int J, bool MM, bool CHECK, int S = num_stages(J)>
 __device__ __forceinline__ void mainloop(const Smem& sm, const CUtensorMap* mapA,
                                          const CUtensorMap* mapB, int m0, int n0, int kt0,
                                          int kt1, Acc<J>& acc, int wm, int wn, int lane, int nvf,
-                                         int mvf, bool& bad) {
-  constexpr int S = num_stages(J);
+                                         int mvf, bool& bad, int mm3d = 0) {
   (void)nvf;
   (void)mvf;
   const int nkt = kt1 - kt0;
@@ -128,13 +139,13 @@ __device__ __forceinline__ void mainloop(const Smem& sm, const CUtensorMap* mapA
   if (leader) {
     tma_prefetch_desc(mapA);
     tma_prefetch_desc(mapB);
-    for (int i = 0; i < S && i < nkt; ++i) issue_stage<J, MM>(sm, mapA, mapB, m0, n0, kt0 + i, i);
+    for (int i = 0; i < S && i < nkt; ++i) issue_stage<J, MM>(sm, mapA, mapB, m0, n0, kt0 + i, i, mm3d);
   }
   const int r8 = lane >> 2, c4 = lane & 3;
   // per-lane element offsets (in doubles) inside one stage
   int offA[2], offB[2];      // KK: chunk offsets for the two k pairs
   int rowA = 0, rowB = 0;    // KK: row bases
-  int mmA[4][4], mmB[4];     // MM: per (s, mi) A offsets; per s B base offsets
+  int mmB[4];                // MM: per k-step B row offsets
   if (!MM) {
 #pragma unroll
     for (int p = 0; p < 2; ++p) {
@@ -145,15 +156,7 @@ __device__ __forceinline__ void mainloop(const Smem& sm, const CUtensorMap* mapA
     rowB = (wn * 8 * J + r8) * 16;
   } else {
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      const int k = s + 4 * c4;
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi) {
-        const int row = wm * 32 + mi * 8 + r8;
-        mmA[s][mi] = (row >> 4) * (16 * BK) + swz128(k, row & 15);
-      }
-      mmB[s] = k * 16;
-    }
+    for (int s = 0; s < 4; ++s) mmB[s] = (s + 4 * c4) * 16;
   }
   for (int i = 0; i < nkt; ++i) {
     const int st = i % S;
@@ -161,7 +164,7 @@ __device__ __forceinline__ void mainloop(const Smem& sm, const CUtensorMap* mapA
     if (leader && i >= 1 && (i - 1) + S < nkt) {
       const int ps = (i - 1) % S;
       mbar_wait(&sm.empty[ps], ((i - 1) / S) & 1);
-      issue_stage<J, MM>(sm, mapA, mapB, m0, n0, kt0 + (i - 1) + S, ps);
+      issue_stage<J, MM>(sm, mapA, mapB, m0, n0, kt0 + (i - 1) + S, ps, mm3d);
     }
     mbar_wait(&sm.full[st], ph);
     const double* sa = sm.a + st * (BM * BK);
@@ -188,13 +191,18 @@ __device__ __forceinline__ void mainloop(const Smem& sm, const CUtensorMap* mapA
           for (int nj = 0; nj < J; ++nj) dmma884(acc.v[mi][nj][0], acc.v[mi][nj][1], a2[mi].y, b2[nj].y);
       }
     } else {
+      // MM: fragment mi = 2q + e of this warp holds output rows
+      // wm*32 + 16q + 2*(lane>>2) + e, so one LDS.128 at (row k, columns
+      // 2*(lane>>2), +1) of box (wm*2 + q) feeds fragments 2q and 2q + 1.
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
-        double af[4], bf[J];
+        const int k = s + 4 * c4;
+        double2 a2[2];
+        double bf[J];
 #pragma unroll
-        for (int mi = 0; mi < 4; ++mi) {
-          af[mi] = sa[mmA[s][mi]];
-          if (CHECK) bad |= is_nonfinite(af[mi]);
+        for (int q = 0; q < 2; ++q) {
+          a2[q] = *reinterpret_cast<const double2*>(sa + (wm * 2 + q) * (16 * BK) + k * 16 + ((r8 ^ (k & 7)) << 1));
+          if (CHECK) bad |= is_nonfinite(a2[q].x) | is_nonfinite(a2[q].y);
         }
 #pragma unroll
         for (int nj = 0; nj < J; ++nj) {
@@ -202,9 +210,12 @@ __device__ __forceinline__ void mainloop(const Smem& sm, const CUtensorMap* mapA
           bf[nj] = sb[(col >> 4) * (16 * BK) + mmB[s] + (((((col & 15) >> 1) ^ ((s + 4 * c4) & 7)) << 1) | (col & 1))];
         }
 #pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-          for (int nj = 0; nj < J; ++nj) dmma884(acc.v[mi][nj][0], acc.v[mi][nj][1], af[mi], bf[nj]);
+        for (int nj = 0; nj < J; ++nj) {
+          dmma884(acc.v[0][nj][0], acc.v[0][nj][1], a2[0].x, bf[nj]);
+          dmma884(acc.v[1][nj][0], acc.v[1][nj][1], a2[0].y, bf[nj]);
+          dmma884(acc.v[2][nj][0], acc.v[2][nj][1], a2[1].x, bf[nj]);
+          dmma884(acc.v[3][nj][0], acc.v[3][nj][1], a2[1].y, bf[nj]);
+        }
       }
     }
     __syncwarp();
@@ -212,9 +223,8 @@ __device__ __forceinline__ void mainloop(const Smem& sm, const CUtensorMap* mapA
   }
 }
 
-template <int J>
+template <int S>
 __device__ __forceinline__ void init_barriers(const Smem& sm) {
-  constexpr int S = num_stages(J);
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
       mbar_init(&sm.full[i], 1);
@@ -238,7 +248,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                 Tile t, StoreParams sp) {
   extern __shared__ unsigned char smem_raw[];
-  Smem sm = carve<J>(smem_raw);
+  Smem sm = carve<J, num_stages(J)>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bid = blockIdx.x;
   const int nt = bid % t.n_tiles;
@@ -248,7 +258,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int n0 = nt * 16 * J;
   const int kt0 = split * t.k_tiles_per_split;
   const int kt1 = min(t.k_tiles, kt0 + t.k_tiles_per_split);
-  init_barriers<J>(sm);
+  init_barriers<num_stages(J)>(sm);
   const int wm = warp & 3, wn = warp >> 2;
   const int ncol0 = n0 + wn * 8 * J;
   const int nvf = max(0, min(J, (t.N - ncol0 + 7) / 8));
@@ -256,7 +266,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   Acc<J> acc;
   acc.zero();
   bool bad = false;
-  mainloop<J, MM, CHECK>(sm, &mapA, &mapB, m0, n0, kt0, kt1, acc, wm, wn, lane, nvf, mvf, bad);
+  mainloop<J, MM, CHECK>(sm, &mapA, &mapB, m0, n0, kt0, kt1, acc, wm, wn, lane, nvf, mvf, bad, t.mm3d);
   if (CHECK && sp.bad_flag) {
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(sp.bad_flag, 1);
   }
@@ -264,7 +274,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int r8 = lane >> 2, c4 = lane & 3;
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi) {
-    const int row = m0 + wm * 32 + mi * 8 + r8;
+    const int row = MM ? m0 + wm * 32 + 16 * (mi >> 1) + 2 * r8 + (mi & 1) : m0 + wm * 32 + mi * 8 + r8;
     if (row >= t.M) continue;
 #pragma unroll
     for (int nj = 0; nj < J; ++nj) {
@@ -293,19 +303,19 @@ struct LrParams {
 };
 
 template <int J, int MODE>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS, 2)
     lowrank_kernel(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapW,
                    Tile t, LrParams p) {
   extern __shared__ unsigned char smem_raw[];
   __shared__ double red_sum[NCW];
   __shared__ long long red_cnt[NCW];
-  Smem sm = carve<J>(smem_raw);
+  Smem sm = carve<J, LR_STAGES, lr_data_bytes(J)>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bid = blockIdx.x;
   const int nt = bid % t.n_tiles;
   const int m0 = (bid / t.n_tiles) * BM;
   const int n0 = nt * 16 * J;
-  init_barriers<J>(sm);
+  init_barriers<LR_STAGES>(sm);
   const int wm = warp & 3, wn = warp >> 2;
   const int ncol0 = n0 + wn * 8 * J;
   const int nvf = max(0, min(J, (t.N - ncol0 + 7) / 8));
@@ -313,7 +323,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   Acc<J> acc;
   acc.zero();
   bool bad = false;
-  mainloop<J, false, false>(sm, &mapU, &mapW, m0, n0, 0, t.k_tiles, acc, wm, wn, lane, nvf, mvf, bad);
+  mainloop<J, false, false, LR_STAGES>(sm, &mapU, &mapW, m0, n0, 0, t.k_tiles, acc, wm, wn, lane, nvf, mvf, bad);
 
   // Stage the 128 x 16J tile of L in shared memory (the pipeline buffers are
   // free now), then stream it row by row: each warp owns rows, lanes cover
