@@ -81,6 +81,16 @@ int corutv_decompose_seeded(corutv_handle* h, const double* a, int64_t m, int64_
                             int ell, int q_power, int variant, const uint64_t* pcg_state, double* u,
                             double* t, double* v, int64_t* perm, int64_t* passes_host);
 
+/* CoR-UTV truncated for the ALM thresholding step (rpca.py:122-132,
+ * _truncate_utv): r = #(|diag T| > delta) is returned in *r_host and the QRCP
+ * stops at step r (|diag T| is non-increasing), so only U[:, :r], T[:r, :]
+ * (rows >= r zeroed), V and perm are formed.  Omega from `omega` (n x ell,
+ * device) or, if NULL, drawn from pcg_state as corutv_decompose_seeded. */
+int corutv_decompose_truncated(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda,
+                               int ell, int q_power, int variant, const double* omega,
+                               const uint64_t* pcg_state, double delta, double* u, double* t,
+                               double* v, int64_t* perm, int64_t* passes_host, int* r_host);
+
 /* np.random.Generator(PCG64(seed)).standard_normal((rows, cols)) into out
  * (row-major, ld) on the device, bit-identical (gaussian_matrix,
  * sketch.py:63-68).  Synchronises the stream. */

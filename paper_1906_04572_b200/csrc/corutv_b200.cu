@@ -548,7 +548,8 @@ double* cholqr(corutv_handle* h, double* xa, double* xb, int64_t rows, int ell, 
 // l <= 32: one CTA (qrcp_kernel).  Larger cores: the thread-block-cluster
 // kernel (qrcp_cluster.cuh) with the core spread over CS CTAs' shared memory.
 void qrcp(corutv_handle* h, const double* D, int l, int64_t ldd, double* T, int64_t ldt, double* qtT,
-          int64_t ldq, long long* perm_out, int* perm32, double* gwork) {
+          int64_t ldq, long long* perm_out, int* perm32, double* gwork, double delta = -1.0,
+          int* r_dev = nullptr) {
   const int optin = max_optin_smem(h);
   // small cores: one CTA with R and Q in shared memory, ~G*l threads
   const size_t one = (size_t)l * l * 8;
@@ -558,7 +559,8 @@ void qrcp(corutv_handle* h, const double* D, int l, int64_t ldd, double* T, int6
     const int threads = (int)std::min<int64_t>(1024, round_up((int64_t)l * G, 32));
     auto kern = (G == 4) ? small::qrcp_kernel<128, 4> : small::qrcp_kernel<128, 2>;
     set_smem(h, kern, 2 * one);
-    kern<<<1, threads, 2 * one, h->stream>>>(D, l, ldd, T, ldt, qtT, ldq, perm_out, perm32, gwork, 1, 1);
+    kern<<<1, threads, 2 * one, h->stream>>>(D, l, ldd, T, ldt, qtT, ldq, perm_out, perm32, gwork, 1, 1, delta,
+                                             r_dev);
     CK_LAUNCH();
     return;
   }
@@ -593,7 +595,7 @@ void qrcp(corutv_handle* h, const double* D, int l, int64_t ldd, double* T, int6
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   CK(cudaLaunchKernelEx(&cfg, qc::qrcp_cluster_kernel, D, l, ldd, cw, T, ldt, qtT, ldq, perm_out, perm32,
-                        gwork, q_smem ? 1 : 0));
+                        gwork, q_smem ? 1 : 0, delta, r_dev));
   ++h->launches;
 }
 
@@ -708,9 +710,12 @@ void gaussian(corutv_handle* h, const uint64_t* pcg, int64_t rows, int64_t cols,
 }
 
 // ------------------------------------------------------------ CoR-UTV
+// delta >= 0: ALM truncation (rpca.py:122-132): the QRCP stops at the first
+// |diag T| <= delta (|diag T| is non-increasing), *r_host = that count, and
+// only U[:, :r] / T[:r, :] are formed (V and perm in full).
 void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, int ell, int q,
                int variant, const double* omega, const uint64_t* pcg, double* u, double* t, double* v,
-               int64_t* perm, int64_t* passes_host) {
+               int64_t* perm, int64_t* passes_host, double delta = -1.0, int* r_host = nullptr) {
   if (!a || (!omega && !pcg) || !u || !t || !v) fail(h, CORUTV_ERR_ARG, "null pointer argument");
   if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
   if (ell < 1) fail(h, CORUTV_ERR_ARG, "ell must be >= 1, got " + std::to_string(ell));
@@ -849,9 +854,18 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
     aux::small_matmul_kernel<<<g, dim3(16, 16), 0, h->stream>>>(B1, ldp, 0, pinvB, ldp, 0, l, l, l, D, ldp);
     CK_LAUNCH();
   }
-  qrcp(h, D, l, ldp, t, l, qtT, ldp, reinterpret_cast<long long*>(perm), perm32, gwork);
-  // lift (sketch.py:205-207)
-  run_gemm(h, false, m, l, l, Q1, ldp, qtT, ldp, u, l, nullptr, 0, ws);
+  int ucols = l;
+  if (delta >= 0.0) {
+    qrcp(h, D, l, ldp, t, l, qtT, ldp, reinterpret_cast<long long*>(perm), perm32, gwork, delta, jstat);
+    CK(cudaMemcpyAsync(h->pinned, jstat, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    sync(h);
+    std::memcpy(&ucols, h->pinned, sizeof(int));
+    if (r_host) *r_host = ucols;
+  } else {
+    qrcp(h, D, l, ldp, t, l, qtT, ldp, reinterpret_cast<long long*>(perm), perm32, gwork);
+  }
+  // lift (sketch.py:205-207); U[:, :r] only when truncating
+  if (ucols > 0) run_gemm(h, false, m, ucols, l, Q1, ldp, qtT, ldp, u, l, nullptr, 0, ws);
   {
     int nb, tb;
     launch_grid_1d(n * l, &nb, &tb);
@@ -1160,6 +1174,22 @@ int corutv_decompose(corutv_handle* hh, const double* a, int64_t m, int64_t n, i
                      int64_t* perm, int64_t* passes_host) {
   ABI_BEGIN(hh)
   decompose(h, a, m, n, lda, ell, q_power, variant, omega, nullptr, u, t, v, perm, passes_host);
+  ABI_END
+}
+
+int corutv_decompose_truncated(corutv_handle* hh, const double* a, int64_t m, int64_t n, int64_t lda, int ell,
+                               int q_power, int variant, const double* omega, const uint64_t* pcg_state,
+                               double delta, double* u, double* t, double* v, int64_t* perm,
+                               int64_t* passes_host, int* r_host) {
+  ABI_BEGIN(hh)
+  if (!(delta >= 0.0)) fail(h, CORUTV_ERR_ARG, "delta must be >= 0");
+  uint64_t st[4] = {0, 0, 0, 0};
+  if (!omega) {
+    if (!pcg_state) fail(h, CORUTV_ERR_ARG, "need omega or pcg_state");
+    for (int i = 0; i < 4; ++i) st[i] = pcg_state[i];
+  }
+  decompose(h, a, m, n, lda, ell, q_power, variant, omega, omega ? nullptr : st, u, t, v, perm, passes_host,
+            delta, r_host);
   ABI_END
 }
 

@@ -116,7 +116,7 @@ __device__ __forceinline__ void issue_stage(const Smem& sm, const CUtensorMap* m
 // in flight: at iteration i it refills the slot released at iteration i-1
 // (waiting on that slot's `empty` barrier, i.e. on the slowest warp), so the
 // wait almost never stalls.  Every warp: wait full -> 4 DMMA k-steps ->
-// arrive empty.  All fragments are computed unconditionally (TMA zero-fills
+// fence -> arrive empty.  All fragments are computed unconditionally (TMA zero-fills
 // out-of-range rows/columns), so the DMMA stream has no predicates.
 //
 // KK: both operands K-major, 128-B rows, 128-B swizzle.  A lane reads the
@@ -218,7 +218,11 @@ __device__ __forceinline__ void mainloop(const Smem& sm, const CUtensorMap* mapA
         }
       }
     }
+    // The fence makes every LDS of this stage complete before the release:
+    // the arrive alone can be scheduled ahead of LDS still queued behind the
+    // DMMAs, and the refill TMA would overwrite bytes not yet read.
     __syncwarp();
+    __threadfence_block();
     if (lane == 0) mbar_arrive(&sm.empty[st]);
   }
 }

@@ -48,7 +48,8 @@ struct Shared {
 __global__ void __launch_bounds__(THREADS, 1)
     qrcp_cluster_kernel(const double* __restrict__ D, int l, int64_t ldd, int cw,
                         double* __restrict__ T, int64_t ldt, double* __restrict__ qtT, int64_t ldq,
-                        long long* perm_out, int* perm32, double* qglobal, int q_in_smem) {
+                        long long* perm_out, int* perm32, double* qglobal, int q_in_smem, double delta,
+                        int* r_out) {
   extern __shared__ double dsm[];
   __shared__ Shared sh;
   cg::cluster_group cluster = cg::this_cluster();
@@ -79,6 +80,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   for (int q = threadIdx.x; q < l; q += THREADS) sh.l2p[0][q] = q;
   cluster.sync();
 
+  int kend = l;
   for (int j = 0; j < l; ++j) {
     const int par = j & 1;
     const int* cur = sh.l2p[par];
@@ -133,8 +135,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     const bool refl = nx != 0.0;
     const double v0 = refl ? x0 + (x0 >= 0.0 ? nx : -nx) : 0.0;
     const double tj = refl ? 2.0 / (v0 * v0 + t2) : 0.0;
+    const double dj = refl ? x0 - v0 * (tj * (v0 * x0 + t2)) : x0;
+    if (delta >= 0.0 && !(fabs(dj) > delta)) {  // identical in every CTA
+      kend = j;
+      break;
+    }
     if (threadIdx.x == 0) {
-      sh.diag[j] = refl ? x0 - v0 * (tj * (v0 * x0 + t2)) : x0;
+      sh.diag[j] = dj;
       sh.tau[j] = tj;
       sh.vhead[j] = v0;
       sh.has_ref[j] = refl;
@@ -170,7 +177,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
   }
   cluster.sync();
-  const int* fin = sh.l2p[l & 1];
+  const int* fin = sh.l2p[kend & 1];
 
   // outputs owned by this CTA: T columns whose pivot column it owns, perm
   for (int cq = warp; cq < l; cq += NW) {
@@ -178,19 +185,21 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (c < c_lo || c >= c_lo + nown) continue;
     const double* col = Rl + (size_t)(c - c_lo) * l;
     for (int i = lane; i < l; i += 32)
-      T[i * ldt + cq] = (i < cq) ? col[i] : ((i == cq) ? sh.diag[cq] : 0.0);
+      T[i * ldt + cq] = (i >= kend) ? 0.0 : ((i < cq) ? col[i] : ((i == cq) ? sh.diag[cq] : 0.0));
   }
-  if (rank == 0)
+  if (rank == 0) {
     for (int c = threadIdx.x; c < l; c += THREADS) {
       if (perm_out) perm_out[c] = fin[c];
       perm32[c] = fin[c];
     }
+    if (threadIdx.x == 0 && r_out) *r_out = kend;
+  }
 
   // explicit Q: this CTA's Q columns [c_lo, c_lo + nown)
   for (int cl = warp; cl < nown; cl += NW)
     for (int i = lane; i < l; i += 32) Ql[(size_t)cl * l + i] = (i == c_lo + cl) ? 1.0 : 0.0;
   __syncthreads();
-  for (int j = l - 1; j >= 0; --j) {
+  for (int j = kend - 1; j >= 0; --j) {
     if (!sh.has_ref[j]) continue;  // uniform
     if (c_lo + nown <= j) continue;  // no owned column c >= j (uniform)
     const int pc = fin[j];

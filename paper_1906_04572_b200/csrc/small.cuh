@@ -337,13 +337,14 @@ __device__ __forceinline__ double group_sum(double v) {
 }
 
 template <int G, int LM>
-__device__ void qrcp_body(double* R, double* Q, int l, double* nrm, double* ref, double* tau,
-                          double* vhead, double* diag, int (*l2p)[LM], int* done, int* has_ref,
-                          const int** fin_out) {
+__device__ int qrcp_body(double* R, double* Q, int l, double* nrm, double* ref, double* tau,
+                         double* vhead, double* diag, int (*l2p)[LM], int* done, int* has_ref,
+                         const int** fin_out, double delta) {
   const int lane = threadIdx.x & 31;
   const int nt = blockDim.x;
   const int gid = threadIdx.x / G, gl = threadIdx.x % G;
   const int ngroups = nt / G;
+  int kend = l;
   for (int j = 0; j < l; ++j) {
     const int* cur = l2p[j & 1];
     int* nxt = l2p[(j + 1) & 1];
@@ -371,9 +372,15 @@ __device__ void qrcp_body(double* R, double* Q, int l, double* nrm, double* ref,
     const bool refl = nx != 0.0;
     const double v0 = refl ? x0 + (x0 >= 0.0 ? nx : -nx) : 0.0;
     const double tj = refl ? 2.0 / (v0 * v0 + t2) : 0.0;
+    const double dj = refl ? x0 - v0 * (tj * (v0 * x0 + t2)) : x0;
+    if (delta >= 0.0 && !(fabs(dj) > delta)) {
+      // |diag T| is non-increasing: r = j (rpca.py:123-124); stop here
+      kend = j;
+      break;
+    }
     for (int q = threadIdx.x; q < l; q += nt) nxt[q] = (q == j) ? cur[p] : ((q == p) ? cur[j] : cur[q]);
     if (threadIdx.x == 0) {
-      diag[j] = refl ? x0 - v0 * (tj * (v0 * x0 + t2)) : x0;
+      diag[j] = dj;
       tau[j] = tj;
       vhead[j] = v0;
       has_ref[j] = refl;
@@ -415,14 +422,15 @@ __device__ void qrcp_body(double* R, double* Q, int l, double* nrm, double* ref,
     if (threadIdx.x == 0) done[pc] = 1;
     __syncthreads();
   }
-  const int* fin = l2p[l & 1];
+  __syncthreads();
+  const int* fin = l2p[kend & 1];
   *fin_out = fin;
 
   // explicit Q by reverse accumulation on the identity (dense.py:117-129)
   for (int i = threadIdx.x >> 5; i < l; i += nt >> 5)
     for (int c = lane; c < l; c += 32) Q[i * l + c] = (i == c) ? 1.0 : 0.0;
   __syncthreads();
-  for (int j = l - 1; j >= 0; --j) {
+  for (int j = kend - 1; j >= 0; --j) {
     if (has_ref[j]) {
       const int pc = fin[j];
       const double v0 = vhead[j], tj = tau[j];
@@ -443,6 +451,7 @@ __device__ void qrcp_body(double* R, double* Q, int l, double* nrm, double* ref,
     }
     __syncthreads();
   }
+  return kend;
 }
 
 // LM: capacity of the per-column arrays (the core must satisfy l <= LM);
@@ -452,7 +461,7 @@ template <int LM, int G>
 __global__ void __launch_bounds__(1024, 1)
     qrcp_kernel(const double* __restrict__ D, int l, int64_t ldd, double* __restrict__ T,
                 int64_t ldt, double* __restrict__ qtT, int64_t ldq, long long* perm_out,
-                int* perm32, double* gwork, int smem_R, int smem_Q) {
+                int* perm32, double* gwork, int smem_R, int smem_Q, double delta, int* r_out) {
   extern __shared__ double dsm[];
   __shared__ double nrm[LM];
   __shared__ double ref[LM];
@@ -484,13 +493,14 @@ __global__ void __launch_bounds__(1024, 1)
   }
   __syncthreads();
   const int* fin = nullptr;
-  qrcp_body<G, LM>(R, Q, l, nrm, ref, tau, vhead, diag, l2p, done, has_ref, &fin);
+  const int kend = qrcp_body<G, LM>(R, Q, l, nrm, ref, tau, vhead, diag, l2p, done, has_ref, &fin, delta);
   __syncthreads();
   for (int i = threadIdx.x >> 5; i < l; i += nt >> 5)
     for (int c = lane; c < l; c += 32) {
-      T[i * ldt + c] = (c > i) ? R[i * l + fin[c]] : ((c == i) ? diag[i] : 0.0);
+      T[i * ldt + c] = (i >= kend) ? 0.0 : ((c > i) ? R[i * l + fin[c]] : ((c == i) ? diag[i] : 0.0));
       qtT[c * ldq + i] = Q[i * l + c];
     }
+  if (threadIdx.x == 0 && r_out) *r_out = kend;
   for (int c = threadIdx.x; c < l; c += nt) {
     if (perm_out) perm_out[c] = fin[c];
     perm32[c] = fin[c];

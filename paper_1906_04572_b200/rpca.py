@@ -25,7 +25,7 @@ from . import _device as dev
 from . import _lib
 from .dense import singular_values, spectral_norm
 from .errors import ConvergenceError
-from .sketch import SketchConfig, corutv
+from .sketch import SketchConfig, corutv, corutv_truncated
 
 __all__ = [
     "AlmConfig",
@@ -129,8 +129,8 @@ def corutv_threshold(b, delta: float, cfg: SketchConfig):
     if delta < 0:
         raise ValueError("delta must be >= 0")
     B, was_host = dev.to_device(b, "b")
-    f = corutv(B, cfg)
-    r = _truncate(f, delta)
+    dev.raise_if_nonfinite(B, "b")
+    f, r = corutv_truncated(B, cfg, delta)
     if r == 0:
         torch = dev.torch_mod()
         return dev.to_output(torch.zeros_like(B), was_host), 0
@@ -172,8 +172,9 @@ def alm_corutv(m, cfg: AlmConfig) -> RpcaSolution:
     nnz = ctypes.c_int64(0)
     for j in range(cfg.max_iter):
         scfg = SketchConfig(ell=cap, q_power=cfg.q_power, seed=(cfg.seed + j) % 2 ** 64)
-        f = corutv(src, scfg)  # Omega = gaussian_matrix(w, cap, seed + j), drawn on the device
-        rank = _truncate(f, 1.0 / mu)
+        # Omega = gaussian_matrix(w, cap, seed + j) drawn on the device; the
+        # rank count r = #(|diag T| > 1/mu) comes back with the factors
+        f, rank = corutv_truncated(src, scfg, 1.0 / mu)
         caps.append(cap)
         cap = _next_cap(cap, rank, limit, grow)
         mu_next = min(cfg.rho * mu, mu_bar)

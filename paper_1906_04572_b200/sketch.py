@@ -195,6 +195,30 @@ def corutv(a, cfg: SketchConfig, counter: PassCounter | None = None, omega=None)
                          variant=cfg.variant, perm=dev.to_output(perm, was_host))
 
 
+def corutv_truncated(A, cfg: SketchConfig, delta: float, counter: PassCounter | None = None):
+    """CoR-UTV of a CUDA tensor for the ALM thresholding step
+    (rpca.py:122-132): returns (factors, r) with r = #(|diag T| > delta); the
+    QRCP stops at step r, so only U[:, :r] and T[:r, :] are formed (the rest
+    of U / T is not meaningful) -- L = U_r (T_r V') is unchanged."""
+    torch = dev.torch_mod()
+    m, n = A.shape
+    ell = cfg.ell
+    u = torch.empty((m, ell), dtype=torch.float64, device=A.device)
+    t = torch.empty((ell, ell), dtype=torch.float64, device=A.device)
+    v = torch.empty((n, ell), dtype=torch.float64, device=A.device)
+    perm = torch.empty((ell,), dtype=torch.int64, device=A.device)
+    passes = ctypes.c_int64(0)
+    r = ctypes.c_int(0)
+    h = _lib.handle(A.device.index)
+    h.call("corutv_decompose_truncated", dev.ptr(A), m, n, A.stride(0), ell, cfg.q_power,
+           _VARIANT_CODE[cfg.variant], None, pcg_state(cfg.seed), float(delta), dev.ptr(u),
+           dev.ptr(t), dev.ptr(v), dev.ptr(perm), ctypes.byref(passes), ctypes.byref(r))
+    if counter is not None:
+        counter.add(passes.value)
+    return CorUtvFactors(u=u, t=t, v=v, ell=ell, q_power=cfg.q_power, variant=cfg.variant,
+                         perm=perm), int(r.value)
+
+
 def corutv_kpq(a, k: int, p: int, q: int, omega=None, seed: int = 0,
                variant: str = VARIANT_EXACT) -> CorUtvFactors:
     """North-star form: target rank k, oversampling p (ell = k + p), q power

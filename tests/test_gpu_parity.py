@@ -428,3 +428,48 @@ def test_corutv_parity_across_ell(decaying_matrix, ell):
     k = ell // 2
     assert np.array_equal(f.perm[:k], ref["perm"][:k])
     assert np.abs(sign_align(f.u[:, :k], ref["u"][:, :k]) - ref["u"][:, :k]).max() <= 1e-9
+
+
+# ------------------------------------------------ low-rank product kernels
+@pytest.mark.parametrize("rows,cols,ell,r", [(130, 70, 5, 3), (1000, 800, 51, 50), (10000, 10000, 51, 50),
+                                             (4096, 4096, 600, 600), (257, 129, 16, 16)])
+def test_lowrank_store_matches_torch(rows, cols, ell, r):
+    """corutv_lowrank (rpca.py:129, L = U_r (T_r V')) against torch."""
+    g = torch.Generator(device="cuda")
+    g.manual_seed(rows + cols + ell)
+    u = torch.randn((rows, ell), generator=g, dtype=torch.float64, device="cuda")
+    t = torch.triu(torch.randn((ell, ell), generator=g, dtype=torch.float64, device="cuda"))
+    v = torch.randn((cols, ell), generator=g, dtype=torch.float64, device="cuda")
+    out = P.rpca._lowrank_device(u, t, v, r)
+    ref = u[:, :r] @ (t[:r, :] @ v.T)
+    assert float((out - ref).norm() / ref.norm()) < 1e-14
+
+
+def test_alm_update_matches_torch_formula():
+    """corutv_alm_update (rpca.py:211-216 fused with rpca.py:129, 208)."""
+    rows, cols, ell, r = 3000, 2000, 40, 30
+    g = torch.Generator(device="cuda")
+    g.manual_seed(9)
+    M = torch.randn((rows, cols), generator=g, dtype=torch.float64, device="cuda")
+    Y = torch.randn((rows, cols), generator=g, dtype=torch.float64, device="cuda")
+    u = torch.randn((rows, ell), generator=g, dtype=torch.float64, device="cuda") * 0.1
+    t = torch.triu(torch.randn((ell, ell), generator=g, dtype=torch.float64, device="cuda"))
+    v = torch.randn((cols, ell), generator=g, dtype=torch.float64, device="cuda") * 0.1
+    mu, lam, mu_next = 0.7, 0.05, 1.05
+    S = torch.empty_like(M); G = torch.empty_like(M); Y2 = Y.clone()
+    import ctypes
+    z2, nnz = ctypes.c_double(0), ctypes.c_int64(0)
+    h = _lib.handle(0)
+    h.call("corutv_alm_update", M.data_ptr(), S.data_ptr(), Y2.data_ptr(), G.data_ptr(), rows, cols,
+           u.data_ptr(), t.data_ptr(), v.data_ptr(), ell, r, mu, lam / mu, mu_next,
+           ctypes.byref(z2), ctypes.byref(nnz))
+    L = u[:, :r] @ (t[:r, :] @ v.T)
+    g2 = M - L + Y / mu
+    s_ref = torch.sign(g2) * torch.clamp_min(g2.abs() - lam / mu, 0.0)
+    z = M - L - s_ref
+    y_ref = Y + mu * z
+    assert float((S - s_ref).abs().max()) < 1e-12
+    assert float((Y2 - y_ref).abs().max()) < 1e-12
+    assert float((G - ((M - s_ref) + y_ref / mu_next)).abs().max()) < 1e-12
+    assert abs(z2.value - float((z * z).sum())) <= 1e-12 * float((z * z).sum())
+    assert nnz.value == int((s_ref.abs() > 1e-12).sum())
