@@ -399,8 +399,10 @@ def main():
                    "h2d_bytes_per_step": int(a_host.numel() * 8),
                    "d2h_bytes_per_step": int(((hi - lo) * ell + ell * ell + n * ell) * 8),
                    "ms_per_step": round(dt * 1e3, 3), "steps": k2,
-                   "path": "paper_1906_04572_b200.corutv(pinned host tensor, SketchConfig(seed=0)) -> H2D of A, "
-                           "device Omega (PCG64+ziggurat), corutv_decompose_seeded, D2H of U,T,V"}
+                   "path": "paper_1906_04572_b200.corutv(pinned host tensor, SketchConfig(seed=0)) -> "
+                           "corutv_decompose_host: A streamed H2D in 1 GiB row chunks, overlapped with the device "
+                           "Omega (PCG64+ziggurat), C1 = A Omega per chunk and the split-K slices of C2 = A' C1; "
+                           "then the resident sweeps; D2H of U,T,V via pinned staging"}
             del a_host
         except RuntimeError as exc:  # e.g. pinned allocation failure
             e2e = {"value": None, "unit": "GFLOP/s", "error": str(exc)[:200],

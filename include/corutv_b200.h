@@ -91,6 +91,18 @@ int corutv_decompose_truncated(corutv_handle* h, const double* a, int64_t m, int
                                const uint64_t* pcg_state, double delta, double* u, double* t,
                                double* v, int64_t* perm, int64_t* passes_host, int* r_host);
 
+/* corutv(a, cfg) for a HOST-resident A (sketch.py:182-208 with the
+ * as_matrix H2D of a numpy input, dense.py:41-50): A (m x n, lda_host;
+ * pinned or pageable) is copied into the caller's device buffer a_dev
+ * (m x ld_dev, 16-byte aligned, ld_dev even) in ~1 GiB row chunks on a copy
+ * stream, and the first sketch sweep C1 = A Omega consumes each chunk as it
+ * lands.  Results are bit-identical to corutv_decompose on the same device
+ * buffer.  Omega from `omega` (device) or, if NULL, from pcg_state. */
+int corutv_decompose_host(corutv_handle* h, const double* a_host, int64_t m, int64_t n,
+                          int64_t lda_host, double* a_dev, int64_t ld_dev, int ell, int q_power,
+                          int variant, const double* omega, const uint64_t* pcg_state, double* u,
+                          double* t, double* v, int64_t* perm, int64_t* passes_host);
+
 /* np.random.Generator(PCG64(seed)).standard_normal((rows, cols)) into out
  * (row-major, ld) on the device, bit-identical (gaussian_matrix,
  * sketch.py:63-68).  Synchronises the stream. */

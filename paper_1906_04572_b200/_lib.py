@@ -40,6 +40,8 @@ SIGNATURES = {
     "corutv_decompose_seeded": (_I32, [_VP, _VP, _I64, _I64, _I64, _I32, _I32, _I32, _VP, _VP, _VP,
                                        _VP, _VP, c_int64_p]),
     "corutv_gaussian": (_I32, [_VP, _VP, _I64, _I64, _VP, _I64]),
+    "corutv_decompose_host": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _I64, _I32, _I32, _I32, _VP, _VP,
+                                     _VP, _VP, _VP, _VP, c_int64_p]),
     "corutv_decompose_truncated": (_I32, [_VP, _VP, _I64, _I64, _I64, _I32, _I32, _I32, _VP, _VP, _D,
                                           _VP, _VP, _VP, _VP, c_int64_p, ctypes.POINTER(_I32)]),
     "corutv_alm_update": (_I32, [_VP, _VP, _VP, _VP, _VP, _I64, _I64, _VP, _VP, _VP, _I32, _I32,

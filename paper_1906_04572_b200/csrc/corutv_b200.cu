@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -44,6 +45,10 @@ struct corutv_handle {
   size_t arena_top = 0;  // Arena stack top (bytes)
   double* pinned = nullptr;  // 64 doubles of pinned host scratch
   int num_sms = 148;
+  // host-input streaming (corutv_decompose_host): copy engine stream and
+  // one event per row chunk
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;
   // profiling (corutv_profile_begin/end): launch counter always on; CUDA
   // events around the DMMA GEMM / low-rank kernels while enabled.
   int64_t launches = 0;
@@ -318,9 +323,11 @@ size_t gemm_ws_elems(const corutv_handle* h, int64_t M, int64_t N, int64_t K) {
 // mm == false: C = A (M x K, lda) * Bt^T, Bt: N x K (ldb)
 // mm == true : C = A^T * B, A: K x M (lda), B: K x N (ldb)
 // C (M x N, ldc) and/or Ct (N x M, ldct).  ws: split-K partial scratch.
+// force: use this plan's split-K partition (a row block of a larger GEMM
+// then gets bit-identical rows).
 void run_gemm(corutv_handle* h, bool mm, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
           const double* B, int64_t ldb, double* C, int64_t ldc, double* Ct, int64_t ldct, double* ws,
-          int* bad_flag = nullptr) {
+          int* bad_flag = nullptr, const GemmPlan* force = nullptr) {
   if (M <= 0 || N <= 0) return;
   int tb, nb;
   if (K <= 0) {
@@ -329,6 +336,10 @@ void run_gemm(corutv_handle* h, bool mm, int64_t M, int64_t N, int64_t K, const 
     return;
   }
   GemmPlan p = plan_gemm(h, M, N, K, true);
+  if (force) {
+    p.splits = force->splits;
+    p.kps = force->kps;
+  }
   gemm::Tile t;
   t.M = (int)M;
   t.N = (int)N;
@@ -375,6 +386,31 @@ void run_gemm(corutv_handle* h, bool mm, int64_t M, int64_t N, int64_t K, const 
     aux::splitk_finalize_kernel<<<nb, tb, 0, h->stream>>>(ws, p.splits, M * ldw, M, N, ldw, C, ldc, Ct, ldct);
     CK_LAUNCH();
   }
+}
+
+// One split-K slice s of `plan` for C = A' B (A: K x M, B: K x N), written as
+// partial s of the split-K workspace layout (ws + s M ldw, ld ldw): the same
+// arithmetic as that slice of the full launch, so a later finalize_splits is
+// bit-identical to run_gemm.  Lets a sweep over row-chunked A start before
+// all of A is resident.
+void run_gemm_mm_split(corutv_handle* h, const GemmPlan& plan, int64_t M, int64_t N, int64_t K, const double* A,
+                       int64_t lda, const double* B, int64_t ldb, double* ws, int s) {
+  const int64_t k0 = (int64_t)s * plan.kps * gemm::BK;
+  const int64_t kn = std::min<int64_t>(K - k0, (int64_t)plan.kps * gemm::BK);
+  const int64_t ldw = round_up(N, 2);
+  GemmPlan one = plan;
+  one.splits = 1;
+  run_gemm(h, true, M, N, kn, A + k0 * lda, lda, B + k0 * ldb, ldb, ws + (int64_t)s * M * ldw, ldw, nullptr, 0,
+           nullptr, nullptr, &one);
+}
+
+void finalize_splits(corutv_handle* h, const GemmPlan& plan, int64_t M, int64_t N, const double* ws, double* C,
+                     int64_t ldc, double* Ct, int64_t ldct) {
+  const int64_t ldw = round_up(N, 2);
+  int nb, tb;
+  launch_grid_1d(M * N, &nb, &tb);
+  aux::splitk_finalize_kernel<<<nb, tb, 0, h->stream>>>(ws, plan.splits, M * ldw, M, N, ldw, C, ldc, Ct, ldct);
+  CK_LAUNCH();
 }
 
 void transpose(corutv_handle* h, const double* src, int64_t rows, int64_t cols, int64_t lds, double* dst,
@@ -713,9 +749,20 @@ void gaussian(corutv_handle* h, const uint64_t* pcg, int64_t rows, int64_t cols,
 // delta >= 0: ALM truncation (rpca.py:122-132): the QRCP stops at the first
 // |diag T| <= delta (|diag T| is non-increasing), *r_host = that count, and
 // only U[:, :r] / T[:r, :] are formed (V and perm in full).
+// Host-resident input (corutv_decompose_host): A is copied into the device
+// buffer `a_dev` (the `a` of decompose) in row chunks on the copy stream, and
+// the first A sweep C1 = A Omega consumes each chunk as soon as it lands, so
+// the H2D transfer overlaps the generation of Omega and the first sweep.
+struct HostFeed {
+  const double* a_host;
+  int64_t ld_host;
+  double* a_dev;
+};
+
 void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, int ell, int q,
                int variant, const double* omega, const uint64_t* pcg, double* u, double* t, double* v,
-               int64_t* perm, int64_t* passes_host, double delta = -1.0, int* r_host = nullptr) {
+               int64_t* perm, int64_t* passes_host, double delta = -1.0, int* r_host = nullptr,
+               const HostFeed* feed = nullptr) {
   if (!a || (!omega && !pcg) || !u || !t || !v) fail(h, CORUTV_ERR_ARG, "null pointer argument");
   if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
   if (ell < 1) fail(h, CORUTV_ERR_ARG, "ell must be >= 1, got " + std::to_string(ell));
@@ -769,12 +816,46 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   wse = std::max(wse, gemm_ws_elems(h, l, l, m));
   wse = std::max(wse, gemm_ws_elems(h, l, l, n));
   ar.add(&ws, wse + 16);
+  // host input: the first A' C1 sweep runs split by split as row chunks land
+  const GemmPlan k2plan = plan_gemm(h, n, l, m, true);
+  double* ws2 = nullptr;
+  if (feed && k2plan.splits > 1) ar.add(&ws2, (size_t)k2plan.splits * n * round_up(l, 2) + 16);
   ar.add(&flag, 4);
   ar.add(&perm32, (size_t)ldp);
   ar.add(&jstat, 4);
   ar.add(&info, 4);
   ar.commit();
 
+  // host input: start the chunked H2D copy before anything else
+  int64_t chunk_rows = 0, n_chunks = 0;
+  auto enqueue_chunk = [&](int64_t c) {
+    const int64_t r0 = c * chunk_rows, rows = std::min(chunk_rows, m - r0);
+    CK(cudaMemcpy2DAsync(feed->a_dev + r0 * lda, (size_t)lda * 8, feed->a_host + r0 * feed->ld_host,
+                         (size_t)feed->ld_host * 8, (size_t)n * 8, (size_t)rows, cudaMemcpyHostToDevice,
+                         h->copy_stream));
+    CK(cudaEventRecord(h->chunk_ev[c], h->copy_stream));
+  };
+  if (feed) {
+    if (!a_ok) fail(h, CORUTV_ERR_ARG, "device buffer for the host input must be 16-byte aligned, even ld");
+    if (!h->copy_stream) CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+    // ~1 GiB chunks (multiples of the 128-row tile); CORUTV_HOST_CHUNK_BYTES
+    // overrides the size (tests use small chunks)
+    int64_t chunk_bytes = (int64_t)1 << 30;
+    if (const char* env = std::getenv("CORUTV_HOST_CHUNK_BYTES")) chunk_bytes = std::max<int64_t>(1, std::atoll(env));
+    chunk_rows = std::max<int64_t>(gemm::BM, chunk_bytes / (8 * n) / gemm::BM * gemm::BM);
+    chunk_rows = std::min(chunk_rows, m);
+    n_chunks = (m + chunk_rows - 1) / chunk_rows;
+    while ((int64_t)h->chunk_ev.size() < n_chunks) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      h->chunk_ev.push_back(e);
+    }
+    // the buffer may be recycled memory: order the copies after the work
+    // already queued on the compute stream
+    CK(cudaEventRecord(h->chunk_ev[0], h->stream));
+    CK(cudaStreamWaitEvent(h->copy_stream, h->chunk_ev[0], 0));
+    enqueue_chunk(0);
+  }
   const double* A = a;
   if (!a_ok) {
     copy2d(h, a, m, n, lda, Apad, ldA);
@@ -793,8 +874,38 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   int cur = 0;
   TagScope* sweep_tag = new TagScope(h, 1);
   for (int it = 0; it <= q; ++it) {
-    run_gemm(h, false, m, l, n, A, ldA, XT, ldn, C1a, ldp, nullptr, 0, ws, it == 0 ? flag : nullptr);
-    if (!sharded) {
+    bool c2_done = false;
+    if (it == 0 && feed) {
+      // row chunks with the full GEMM's split-K partition: bit-identical C1;
+      // each split-K slice of C2 = A' C1 starts once its rows are in
+      const GemmPlan full = plan_gemm(h, m, l, n, true);
+      const int64_t split_rows = (int64_t)k2plan.kps * gemm::BK;
+      int next_split = 0;
+      for (int64_t c = 0; c < n_chunks; ++c) {
+        if (c + 1 < n_chunks) enqueue_chunk(c + 1);
+        CK(cudaStreamWaitEvent(h->stream, h->chunk_ev[c], 0));
+        const int64_t r0 = c * chunk_rows, rows = std::min(chunk_rows, m - r0);
+        run_gemm(h, false, rows, l, n, A + r0 * ldA, ldA, XT, ldn, C1a + r0 * ldp, ldp, nullptr, 0, ws, flag,
+                 &full);
+        while (ws2 && next_split < k2plan.splits &&
+               r0 + rows >= std::min<int64_t>(m, (int64_t)(next_split + 1) * split_rows)) {
+          run_gemm_mm_split(h, k2plan, n, l, m, A, ldA, C1a, ldp, ws2, next_split);
+          ++next_split;
+        }
+      }
+      if (ws2) {
+        finalize_splits(h, k2plan, n, l, ws2, Xn[cur ^ 1], ldp, (!sharded && it < q) ? XT : nullptr, ldn);
+        if (sharded) {
+          allreduce(h, Xn[cur ^ 1], n * ldp);
+          if (it < q) transpose(h, Xn[cur ^ 1], n, l, ldp, XT, ldn);
+        }
+        c2_done = true;
+      }
+    } else {
+      run_gemm(h, false, m, l, n, A, ldA, XT, ldn, C1a, ldp, nullptr, 0, ws, it == 0 ? flag : nullptr);
+    }
+    if (c2_done) {
+    } else if (!sharded) {
       run_gemm(h, true, n, l, m, A, ldA, C1a, ldp, Xn[cur ^ 1], ldp, it < q ? XT : nullptr, ldn, ws);
     } else {
       run_gemm(h, true, n, l, m, A, ldA, C1a, ldp, Xn[cur ^ 1], ldp, nullptr, 0, ws);
@@ -1149,6 +1260,8 @@ void corutv_destroy(corutv_handle* h) {
   else cudaDeviceSynchronize();
   if (h->arena) cudaFree(h->arena);
   if (h->pinned) cudaFreeHost(h->pinned);
+  for (cudaEvent_t e : h->chunk_ev) cudaEventDestroy(e);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   delete h;
 }
 
@@ -1200,6 +1313,25 @@ int corutv_decompose_seeded(corutv_handle* hh, const double* a, int64_t m, int64
   if (!pcg_state) fail(h, CORUTV_ERR_ARG, "null pcg_state");
   uint64_t st[4] = {pcg_state[0], pcg_state[1], pcg_state[2], pcg_state[3]};
   decompose(h, a, m, n, lda, ell, q_power, variant, nullptr, st, u, t, v, perm, passes_host);
+  ABI_END
+}
+
+int corutv_decompose_host(corutv_handle* hh, const double* a_host, int64_t m, int64_t n, int64_t lda_host,
+                          double* a_dev, int64_t ld_dev, int ell, int q_power, int variant, const double* omega,
+                          const uint64_t* pcg_state, double* u, double* t, double* v, int64_t* perm,
+                          int64_t* passes_host) {
+  ABI_BEGIN(hh)
+  if (!a_host || !a_dev) fail(h, CORUTV_ERR_ARG, "null pointer argument");
+  if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
+  if (lda_host < n || ld_dev < n) fail(h, CORUTV_ERR_ARG, "leading dimension < n");
+  uint64_t st[4] = {0, 0, 0, 0};
+  if (!omega) {
+    if (!pcg_state) fail(h, CORUTV_ERR_ARG, "need omega or pcg_state");
+    for (int i = 0; i < 4; ++i) st[i] = pcg_state[i];
+  }
+  HostFeed feed{a_host, lda_host, a_dev};
+  decompose(h, a_dev, m, n, ld_dev, ell, q_power, variant, omega, omega ? nullptr : st, u, t, v, perm,
+            passes_host, -1.0, nullptr, &feed);
   ABI_END
 }
 

@@ -204,10 +204,20 @@ __device__ __forceinline__ void mainloop(const Smem& sm, const CUtensorMap* mapA
           a2[q] = *reinterpret_cast<const double2*>(sa + (wm * 2 + q) * (16 * BK) + k * 16 + ((r8 ^ (k & 7)) << 1));
           if (CHECK) bad |= is_nonfinite(a2[q].x) | is_nonfinite(a2[q].y);
         }
+        // B: fragments 2p and 2p+1 hold columns 16p + 2(lane>>2) + {0, 1}
+        // of the warp's slice, so one LDS.128 feeds both; an odd
+        // last fragment keeps the plain column order.
 #pragma unroll
-        for (int nj = 0; nj < J; ++nj) {
-          const int col = wn * 8 * J + nj * 8 + r8;
-          bf[nj] = sb[(col >> 4) * (16 * BK) + mmB[s] + (((((col & 15) >> 1) ^ ((s + 4 * c4) & 7)) << 1) | (col & 1))];
+        for (int pq = 0; pq < J / 2; ++pq) {
+          const int col = wn * 8 * J + pq * 16 + 2 * r8;
+          const double2 b2 = *reinterpret_cast<const double2*>(
+              sb + (col >> 4) * (16 * BK) + mmB[s] + ((((col & 15) >> 1) ^ (k & 7)) << 1));
+          bf[2 * pq] = b2.x;
+          bf[2 * pq + 1] = b2.y;
+        }
+        if (J & 1) {
+          const int col = wn * 8 * J + (J - 1) * 8 + r8;
+          bf[J - 1] = sb[(col >> 4) * (16 * BK) + mmB[s] + (((((col & 15) >> 1) ^ (k & 7)) << 1) | (col & 1))];
         }
 #pragma unroll
         for (int nj = 0; nj < J; ++nj) {
@@ -275,17 +285,34 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(sp.bad_flag, 1);
   }
   double* out = sp.c + (int64_t)split * sp.split_stride;
+  const bool vec = ((sp.ldc & 1) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
   const int r8 = lane >> 2, c4 = lane & 3;
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi) {
     const int row = MM ? m0 + wm * 32 + 16 * (mi >> 1) + 2 * r8 + (mi & 1) : m0 + wm * 32 + mi * 8 + r8;
     if (row >= t.M) continue;
+    double* rowp = out + (int64_t)row * sp.ldc;
 #pragma unroll
     for (int nj = 0; nj < J; ++nj) {
-      const int col = ncol0 + nj * 8 + 2 * c4;
-      double* p = out + (int64_t)row * sp.ldc + col;
-      if (col < t.N) p[0] = acc.v[mi][nj][0];
-      if (col + 1 < t.N) p[1] = acc.v[mi][nj][1];
+      if (MM && nj < (J & ~1)) {
+        // paired fragments (see mainloop): element e of fragment 2p+h sits
+        // at column 16p + 4(lane&3) + 2e + h
+        if (nj & 1) continue;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = ncol0 + (nj >> 1) * 16 + 4 * c4 + 2 * e;
+          if (vec && col + 1 < t.N) {
+            *reinterpret_cast<double2*>(rowp + col) = make_double2(acc.v[mi][nj][e], acc.v[mi][nj + 1][e]);
+          } else {
+            if (col < t.N) rowp[col] = acc.v[mi][nj][e];
+            if (col + 1 < t.N) rowp[col + 1] = acc.v[mi][nj + 1][e];
+          }
+        }
+      } else {
+        const int col = ncol0 + nj * 8 + 2 * c4;
+        if (col < t.N) rowp[col] = acc.v[mi][nj][0];
+        if (col + 1 < t.N) rowp[col + 1] = acc.v[mi][nj][1];
+      }
     }
   }
 }

@@ -170,6 +170,8 @@ def corutv(a, cfg: SketchConfig, counter: PassCounter | None = None, omega=None)
         if m < n:
             raise ValueError(f"corutv requires rows >= cols, got {m}x{n}")
         cfg.validated_for(m, n)
+    if not dev.is_device_tensor(a):
+        return _corutv_host(a, cfg, counter, omega)
     A, was_host = dev.to_device(a, "a")
     ell = cfg.ell
     u = torch.empty((m, ell), dtype=torch.float64, device=A.device)
@@ -193,6 +195,52 @@ def corutv(a, cfg: SketchConfig, counter: PassCounter | None = None, omega=None)
     return CorUtvFactors(u=dev.to_output(u, was_host), t=dev.to_output(t, was_host),
                          v=dev.to_output(v, was_host), ell=ell, q_power=cfg.q_power,
                          variant=cfg.variant, perm=dev.to_output(perm, was_host))
+
+
+def _corutv_host(a, cfg: SketchConfig, counter: PassCounter | None, omega) -> CorUtvFactors:
+    """corutv of a host-resident matrix: the library streams A into a device
+    buffer in row chunks and overlaps the copy with Omega and the first
+    sketch sweep (corutv_decompose_host); results are bit-identical to the
+    device-resident call.  Factors come back as numpy arrays (host torch
+    tensors for a host torch input)."""
+    torch = dev.torch_mod()
+    if dev.is_host_tensor(a):
+        src = a if (a.dtype == torch.float64 and a.stride(1) == 1) else a.to(torch.float64).contiguous()
+        host_ptr, ld_host, kind = src.data_ptr(), src.stride(0), "torch"
+    else:
+        src = np.ascontiguousarray(a, dtype=np.float64)
+        host_ptr, ld_host, kind = src.ctypes.data, src.shape[1], True
+    m, n = src.shape
+    ell = cfg.ell
+    device = torch.device("cuda", torch.cuda.current_device())
+    ld_dev = n + (n & 1)
+    a_dev = torch.empty((m, ld_dev), dtype=torch.float64, device=device)
+    u = torch.empty((m, ell), dtype=torch.float64, device=device)
+    t = torch.empty((ell, ell), dtype=torch.float64, device=device)
+    v = torch.empty((n, ell), dtype=torch.float64, device=device)
+    perm = torch.empty((ell,), dtype=torch.int64, device=device)
+    passes = ctypes.c_int64(0)
+    h = _lib.handle(device.index)
+    om = None if omega is None else _omega_device(omega, n, ell, cfg.seed, a_dev)
+    h.call("corutv_decompose_host", host_ptr, m, n, ld_host, dev.ptr(a_dev), ld_dev, ell, cfg.q_power,
+           _VARIANT_CODE[cfg.variant], None if om is None else dev.ptr(om),
+           None if om is not None else pcg_state(cfg.seed), dev.ptr(u), dev.ptr(t), dev.ptr(v),
+           dev.ptr(perm), ctypes.byref(passes))
+    del src
+    if counter is not None:
+        counter.add(passes.value)
+    # factors come back through pinned staging (torch's host caching
+    # allocator recycles the blocks call to call)
+    outs = []
+    for x in (u, t, v, perm):
+        y = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+        y.copy_(x, non_blocking=True)
+        outs.append(y)
+    torch.cuda.current_stream(device).synchronize()
+    if kind is True:
+        outs = [y.numpy() for y in outs]
+    return CorUtvFactors(u=outs[0], t=outs[1], v=outs[2], ell=ell, q_power=cfg.q_power, variant=cfg.variant,
+                         perm=outs[3])
 
 
 def corutv_truncated(A, cfg: SketchConfig, delta: float, counter: PassCounter | None = None):

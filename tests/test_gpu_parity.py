@@ -50,7 +50,8 @@ def check_factors(f, a, ell, tol=1e-10):
 @pytest.mark.parametrize("trans", [0, 1])
 @pytest.mark.parametrize("shape", [(1, 1, 1), (7, 3, 5), (130, 15, 33), (1000, 15, 1000),
                                    (4000, 50, 3000), (520, 110, 700), (300, 272, 513),
-                                   (64, 600, 200), (257, 129, 4097)])
+                                   (64, 600, 200), (257, 129, 4097), (96, 16, 64), (200, 32, 300),
+                                   (1000, 112, 800), (333, 80, 96)])
 def test_gemm_matches_numpy(trans, shape):
     M, N, K = shape
     rng = np.random.Generator(np.random.PCG64(M * 7 + N + K))
@@ -177,6 +178,41 @@ def test_device_tensor_in_device_tensor_out(golden):
     assert np.array_equal(f.t.cpu().numpy(), g.t)
     L = f.lowrank()
     assert L.is_cuda and np.abs(L.cpu().numpy() - g.lowrank()).max() < 1e-12
+
+
+@pytest.mark.parametrize("chunk_bytes", [None, 1 << 20, 300000])
+@pytest.mark.parametrize("shape,ell,q", [((3000, 500), 40, 2), ((2049, 333), 17, 0), ((1000, 999), 50, 1)])
+def test_host_input_streamed_is_bitwise_device_path(monkeypatch, chunk_bytes, shape, ell, q):
+    """corutv of a host matrix (chunked H2D overlapped with the first sweep,
+    corutv_decompose_host) == corutv of the same matrix already on the device."""
+    if chunk_bytes is not None:
+        monkeypatch.setenv("CORUTV_HOST_CHUNK_BYTES", str(chunk_bytes))
+    rng = np.random.Generator(np.random.PCG64(shape[0] + ell))
+    m, n = shape
+    a = rng.standard_normal((m, 30)) @ rng.standard_normal((30, n)) + 1e-3 * rng.standard_normal((m, n))
+    for variant in (P.VARIANT_EXACT, P.VARIANT_APPROX):
+        cfg = P.SketchConfig(ell=ell, q_power=q, seed=5, variant=variant)
+        fd = P.corutv(torch.from_numpy(a).cuda(), cfg)
+        cnt = P.PassCounter()
+        fh = P.corutv(a, cfg, cnt)
+        assert isinstance(fh.u, np.ndarray)
+        assert cnt.passes == 2 * (q + 1) + (1 if variant == P.VARIANT_EXACT else 0)  # sketch.py:169-203
+        for x, y in ((fh.u, fd.u), (fh.t, fd.t), (fh.v, fd.v), (fh.perm, fd.perm)):
+            assert np.array_equal(x, y.cpu().numpy())
+    # pinned host torch tensor in -> host torch tensors out
+    ah = torch.from_numpy(a).pin_memory()
+    ft = P.corutv(ah, cfg)
+    assert isinstance(ft.t, torch.Tensor) and not ft.t.is_cuda
+    assert np.array_equal(ft.t.numpy(), fd.t.cpu().numpy())
+
+
+def test_host_input_nonfinite_raises(monkeypatch):
+    monkeypatch.setenv("CORUTV_HOST_CHUNK_BYTES", str(1 << 20))
+    rng = np.random.Generator(np.random.PCG64(8))
+    a = rng.standard_normal((3000, 400))
+    a[2900, 7] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        P.corutv(a, P.SketchConfig(ell=10))
 
 
 def test_strided_device_view():
