@@ -41,8 +41,18 @@ __global__ void splitk_finalize_kernel(const double* __restrict__ ws, int splits
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = idx / N, j = idx % N;
+    // fixed summation order; loads batched so they are in flight together
+    const double* src = ws + i * ldw + j;
     double s = 0.0;
-    for (int k = 0; k < splits; ++k) s += ws[k * split_stride + i * ldw + j];
+    int k = 0;
+    for (; k + 16 <= splits; k += 16) {
+      double v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = src[(int64_t)(k + u) * split_stride];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) s += v[u];
+    }
+    for (; k < splits; ++k) s += src[(int64_t)k * split_stride];
     if (C) C[i * ldc + j] = s;
     if (Ct) Ct[j * ldct + i] = s;
   }

@@ -1189,7 +1189,8 @@ void spectral_norm(corutv_handle* h, const double* a, int64_t m, int64_t n, int6
     // est = sigma_1(w) = sqrt(lambda_max(w'w))
     run_gemm(h, true, b, b, mp, w, ldb2, w, ldb2, G, ldb2, nullptr, 0, ws);
     if (sharded) allreduce(h, G, (int64_t)b * ldb2);
-    jacobi(h, G, b, b, ldb2, sig, nullptr, 0, gwork, st);
+    small::sym_lmax_kernel<<<1, 32, 0, h->stream>>>(G, b, ldb2, sig);
+    CK_LAUNCH();
     CK(cudaMemcpyAsync(h->pinned, sig, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     sync(h);
     const double est = std::sqrt(std::max(h->pinned[0], 0.0));

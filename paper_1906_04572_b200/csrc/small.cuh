@@ -634,4 +634,101 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (threadIdx.x == 0 && status) *status = st;
 }
 
+// Largest eigenvalue of a symmetric b x b matrix G (b <= 32; the lower
+// triangle is read), one warp: Householder tridiagonalisation (LAPACK
+// dsytd2 / dlarfg conventions) then multisection on the tridiagonal with
+// Sturm counts, 32 shifts per step.  Both stages are backward stable, so
+// lambda_max is accurate to a few u ||G|| -- what the block power iteration
+// of spectral_norm needs from sigma_1(w)^2 = lambda_max(w'w) (dense.py:425-431
+// takes sigma_1 of the QR factor of w; same value to rounding).
+__global__ void __launch_bounds__(32) sym_lmax_kernel(const double* __restrict__ G, int b, int64_t ldg,
+                                                      double* __restrict__ out) {
+  __shared__ double A[32][33];
+  __shared__ double vs[32], ws[32], d[32], e[32];
+  const int lane = threadIdx.x;
+  for (int j = 0; j < b; ++j)
+    if (lane < b) A[lane][j] = (lane >= j) ? G[lane * ldg + j] : G[j * ldg + lane];
+  __syncwarp();
+  for (int k = 0; k + 2 < b; ++k) {
+    // reflector for x = A[k+1:b, k]:  H x = beta e1, H = I - tau v v', v[0] = 1
+    const double alpha = A[k + 1][k];
+    const double xt = (lane > k + 1 && lane < b) ? A[lane][k] : 0.0;
+    const double sigma = warp_sum(xt * xt);
+    d[k] = A[k][k];
+    if (sigma == 0.0) {
+      if (lane == 0) e[k] = alpha;
+      __syncwarp();
+      continue;
+    }
+    const double nrm = sqrt(alpha * alpha + sigma);
+    const double beta = (alpha >= 0.0) ? -nrm : nrm;
+    const double tau = (beta - alpha) / beta;
+    const double scal = 1.0 / (alpha - beta);
+    const double vi = (lane == k + 1) ? 1.0 : ((lane > k + 1 && lane < b) ? A[lane][k] * scal : 0.0);
+    vs[lane] = vi;
+    if (lane == 0) e[k] = beta;
+    __syncwarp();
+    // p = tau A22 v ; w = p - (tau/2)(p'v) v ; A22 -= v w' + w v'
+    double pi = 0.0;
+    if (lane > k && lane < b)
+      for (int j = k + 1; j < b; ++j) pi = fma(A[lane][j], vs[j], pi);
+    pi *= tau;
+    const double kk = -0.5 * tau * warp_sum(pi * vi);
+    const double wi = fma(kk, vi, pi);
+    ws[lane] = wi;
+    __syncwarp();
+    if (lane > k && lane < b)
+      for (int j = k + 1; j < b; ++j) A[lane][j] -= vi * ws[j] + wi * vs[j];
+    __syncwarp();
+  }
+  if (lane == 0) {
+    if (b >= 2) {
+      d[b - 2] = A[b - 2][b - 2];
+      e[b - 2] = A[b - 1][b - 2];
+    }
+    d[b - 1] = A[b - 1][b - 1];
+  }
+  __syncwarp();
+  // Gershgorin bracket of lambda_max
+  double lo = 1e308, hi = -1e308, emax2 = 0.0;
+  for (int i = 0; i < b; ++i) {
+    const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < b ? fabs(e[i]) : 0.0);
+    lo = fmin(lo, d[i] - r);
+    hi = fmax(hi, d[i] + r);
+    if (i + 1 < b) emax2 = fmax(emax2, e[i] * e[i]);
+  }
+  const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax2);
+  const double span = fmax(fabs(lo), fabs(hi));
+  lo -= 4.0 * 2.220446049250313e-16 * span + pivmin;
+  hi += 4.0 * 2.220446049250313e-16 * span + pivmin;
+  // multisection: count(x) = #eigenvalues < x; lambda_max in [lo, hi)
+  for (int step = 0; step < 64; ++step) {
+    const double x = lo + (hi - lo) * ((double)(lane + 1) / 33.0);
+    int cnt = 0;
+    double q = d[0] - x;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += (q < 0.0);
+    for (int i = 1; i < b; ++i) {
+      q = (d[i] - x) - e[i - 1] * e[i - 1] / q;
+      if (fabs(q) < pivmin) q = -pivmin;
+      cnt += (q < 0.0);
+    }
+    // smallest shift above lambda_max (cnt == b)
+    const unsigned above = __ballot_sync(0xffffffffu, cnt == b);
+    double nlo = lo, nhi = hi;
+    if (above) {
+      const int f = __ffs(above) - 1;
+      nhi = __shfl_sync(0xffffffffu, x, f);
+      if (f > 0) nlo = __shfl_sync(0xffffffffu, x, f - 1);
+    } else {
+      nlo = __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (nlo == lo && nhi == hi) break;
+    lo = nlo;
+    hi = nhi;
+    if (hi - lo <= 2.220446049250313e-16 * fmax(fabs(lo), fabs(hi))) break;
+  }
+  if (lane == 0) out[0] = 0.5 * (lo + hi);
+}
+
 }  // namespace small

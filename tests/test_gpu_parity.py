@@ -308,6 +308,25 @@ def test_spectral_norm_wide_and_iters():
     assert abs(it - oit) <= 1
 
 
+@pytest.mark.parametrize("kind", ["repeated", "graded", "rank1", "cluster"])
+def test_spectral_norm_block_power_spectra(kind):
+    """Block power iteration (lambda_max of the b x b Gram by tridiagonal
+    multisection) against the oracle on spectra that stress the eigen step."""
+    rng = np.random.Generator(np.random.PCG64(len(kind)))
+    m, n = 300, 200
+    qu, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    qv, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    sig = {"repeated": np.r_[np.full(5, 3.0), np.linspace(1.0, 0.1, n - 5)],
+           "graded": 10.0 ** -np.linspace(0, 12, n),
+           "rank1": np.r_[7.0, np.zeros(n - 1)],
+           "cluster": np.r_[2.0, 2.0 - 1e-9, np.linspace(1.0, 0.5, n - 2)]}[kind]
+    a = (qu * sig) @ qv.T
+    val, it = P.dense.spectral_norm_iters(a)
+    oval, oit = O.spectral_norm(a)
+    assert abs(val - oval) <= 1e-12 * oval
+    assert abs(it - oit) <= 1
+
+
 def test_singular_values_golden(golden):
     c = golden["sv"]
     assert np.abs(P.singular_values(c["a"]) - c["sig"]).max() <= 1e-13 * c["sig"][0]
