@@ -379,72 +379,81 @@ __global__ void __launch_bounds__(THREADS, 2)
   long long cnt = 0;
   const int ncols = min(TN, t.N - n0);
   const bool vec = ((p.ld & 1) == 0);
-  for (int rb = warp * 4; rb < BM; rb += NCW * 4) {
+  // Each warp owns rows {4w .. 4w+3} + 32k; a batch of RB rows has all its
+  // M / Y loads issued before any store (Y is read and written, so loads
+  // of later rows could not otherwise move above earlier stores), keeping
+  // RB x 2 x 512 B per warp in flight.  TN <= 64: one double2 per lane.
+  constexpr int RB = 8;
+  const int c = 2 * lane;
+  const bool pair = vec && (c + 1 < ncols);
+  for (int base = warp * 4; base < BM; base += NCW * 4 * (RB / 4)) {
+    double2 mv[RB], yv[RB];
 #pragma unroll
-    for (int rr = 0; rr < 4; ++rr) {
-      const int row = rb + rr;
+    for (int q = 0; q < RB; ++q) {
+      const int row = base + (q >> 2) * (NCW * 4) + (q & 3);
       const int grow = m0 + row;
-      if (grow >= t.M) continue;
-      for (int c = 2 * lane; c < ncols; c += 64) {
+      mv[q] = make_double2(0.0, 0.0);
+      yv[q] = make_double2(0.0, 0.0);
+      if (MODE != LR_STORE && row < BM && grow < t.M && c < ncols) {
         const int64_t idx = (int64_t)grow * p.ld + n0 + c;
-        const double2 l2 = *reinterpret_cast<const double2*>(tileL + row * LDT + c);
-        const bool pair = vec && (c + 1 < ncols);
-        double lv[2] = {l2.x, l2.y};
-        double mv[2] = {0.0, 0.0}, yv[2] = {0.0, 0.0};
-        if (MODE != LR_STORE) {
-          if (pair) {
-            const double2 m2 = *reinterpret_cast<const double2*>(p.m_mat + idx);
-            mv[0] = m2.x; mv[1] = m2.y;
-            if (MODE == LR_ALM) {
-              const double2 y2 = *reinterpret_cast<const double2*>(p.y + idx);
-              yv[0] = y2.x; yv[1] = y2.y;
-            }
-          } else {
-            mv[0] = p.m_mat[idx];
-            if (c + 1 < ncols) mv[1] = p.m_mat[idx + 1];
-            if (MODE == LR_ALM) {
-              yv[0] = p.y[idx];
-              if (c + 1 < ncols) yv[1] = p.y[idx + 1];
-            }
+        if (pair) {
+          mv[q] = *reinterpret_cast<const double2*>(p.m_mat + idx);
+          if (MODE == LR_ALM) yv[q] = *reinterpret_cast<const double2*>(p.y + idx);
+        } else {
+          mv[q].x = p.m_mat[idx];
+          if (c + 1 < ncols) mv[q].y = p.m_mat[idx + 1];
+          if (MODE == LR_ALM) {
+            yv[q].x = p.y[idx];
+            if (c + 1 < ncols) yv[q].y = p.y[idx + 1];
           }
         }
-        double sv[2], yn[2], gv[2];
+      }
+    }
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          if (e == 1 && c + 1 >= ncols) continue;
-          const double l = lv[e];
-          if (MODE == LR_RESID) {
-            const double d = mv[e] - l;
-            ssum = fma(d, d, ssum);
-          } else if (MODE == LR_ALM) {
-            // rpca.py:211-214, operation order mirrored from the numpy source
-            const double mm = mv[e], yy = yv[e];
-            const double g = (mm - l) + yy / p.mu;
-            const double ag = fabs(g) - p.lam_over_mu;
-            const double sg = (g > 0.0) ? 1.0 : ((g < 0.0) ? -1.0 : g);
-            sv[e] = sg * fmax(ag, 0.0);
-            const double z = (mm - l) - sv[e];
-            yn[e] = yy + p.mu * z;
-            gv[e] = (mm - sv[e]) + yn[e] / p.mu_next;
-            ssum = fma(z, z, ssum);
-            cnt += (fabs(sv[e]) > 1e-12) ? 1 : 0;
-          }
-        }
-        if (MODE == LR_STORE) {
-          if (pair) *reinterpret_cast<double2*>(p.g_next + idx) = make_double2(lv[0], lv[1]);
-          else {
-            p.g_next[idx] = lv[0];
-            if (c + 1 < ncols) p.g_next[idx + 1] = lv[1];
-          }
+    for (int q = 0; q < RB; ++q) {
+      const int row = base + (q >> 2) * (NCW * 4) + (q & 3);
+      const int grow = m0 + row;
+      if (row >= BM || grow >= t.M || c >= ncols) continue;
+      const int64_t idx = (int64_t)grow * p.ld + n0 + c;
+      const double2 l2 = *reinterpret_cast<const double2*>(tileL + row * LDT + c);
+      const double lv[2] = {l2.x, l2.y};
+      const double mvv[2] = {mv[q].x, mv[q].y}, yvv[2] = {yv[q].x, yv[q].y};
+      double sv[2], yn[2], gv[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (e == 1 && c + 1 >= ncols) continue;
+        const double l = lv[e];
+        if (MODE == LR_RESID) {
+          const double d = mvv[e] - l;
+          ssum = fma(d, d, ssum);
         } else if (MODE == LR_ALM) {
-          if (pair) {
-            *reinterpret_cast<double2*>(p.s + idx) = make_double2(sv[0], sv[1]);
-            *reinterpret_cast<double2*>(p.y + idx) = make_double2(yn[0], yn[1]);
-            *reinterpret_cast<double2*>(p.g_next + idx) = make_double2(gv[0], gv[1]);
-          } else {
-            p.s[idx] = sv[0]; p.y[idx] = yn[0]; p.g_next[idx] = gv[0];
-            if (c + 1 < ncols) { p.s[idx + 1] = sv[1]; p.y[idx + 1] = yn[1]; p.g_next[idx + 1] = gv[1]; }
-          }
+          // rpca.py:211-214, operation order mirrored from the numpy source
+          const double mm = mvv[e], yy = yvv[e];
+          const double g = (mm - l) + yy / p.mu;
+          const double ag = fabs(g) - p.lam_over_mu;
+          const double sg = (g > 0.0) ? 1.0 : ((g < 0.0) ? -1.0 : g);
+          sv[e] = sg * fmax(ag, 0.0);
+          const double z = (mm - l) - sv[e];
+          yn[e] = yy + p.mu * z;
+          gv[e] = (mm - sv[e]) + yn[e] / p.mu_next;
+          ssum = fma(z, z, ssum);
+          cnt += (fabs(sv[e]) > 1e-12) ? 1 : 0;
+        }
+      }
+      if (MODE == LR_STORE) {
+        if (pair) *reinterpret_cast<double2*>(p.g_next + idx) = make_double2(lv[0], lv[1]);
+        else {
+          p.g_next[idx] = lv[0];
+          if (c + 1 < ncols) p.g_next[idx + 1] = lv[1];
+        }
+      } else if (MODE == LR_ALM) {
+        if (pair) {
+          *reinterpret_cast<double2*>(p.s + idx) = make_double2(sv[0], sv[1]);
+          *reinterpret_cast<double2*>(p.y + idx) = make_double2(yn[0], yn[1]);
+          *reinterpret_cast<double2*>(p.g_next + idx) = make_double2(gv[0], gv[1]);
+        } else {
+          p.s[idx] = sv[0]; p.y[idx] = yn[0]; p.g_next[idx] = gv[0];
+          if (c + 1 < ncols) { p.s[idx + 1] = sv[1]; p.y[idx + 1] = yn[1]; p.g_next[idx + 1] = gv[1]; }
         }
       }
     }
