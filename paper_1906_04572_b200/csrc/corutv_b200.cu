@@ -360,6 +360,11 @@ void run_gemm(corutv_handle* h, bool mm, int64_t M, int64_t N, int64_t K, const 
     ma = make_map(h, A, M, K, lda, gemm::BK);
     mb = make_map(h, B, N, K, ldb, gemm::BK);
   }
+  static const bool debug_plan = std::getenv("CORUTV_DEBUG_PLAN") != nullptr;
+  if (debug_plan)
+    std::fprintf(stderr, "[corutv] gemm %s M=%lld N=%lld K=%lld J=%d tiles=%dx%d splits=%d kps=%d mm3d=%d\n",
+                 mm ? "MM" : "KK", (long long)M, (long long)N, (long long)K, p.J, p.m_tiles, p.n_tiles, p.splits,
+                 p.kps, t.mm3d);
   const bool direct = (p.splits == 1 && Ct == nullptr && C != nullptr);
   const int64_t ldw = round_up(N, 2);
   gemm::StoreParams sp;

@@ -9,12 +9,14 @@ torch.cuda.set_device(0)
 m, n, ell = 131072, 32768, 110
 A = bench.gen_rows_device(torch, "c3", 0, m, torch.device("cuda", 0))
 X = torch.randn(n, ell, dtype=torch.float64, device='cuda')
-Y = torch.randn(m, ell, dtype=torch.float64, device='cuda')
+# C1 as the decompose lays it out: ld = round_up(ell, 16) (3-D TMA boxes)
+Yp = torch.randn(m, 112, dtype=torch.float64, device='cuda')
+Y = Yp[:, :ell]
 C1 = torch.empty(m, ell, dtype=torch.float64, device='cuda')
 C2 = torch.empty(n, ell, dtype=torch.float64, device='cuda')
 torch.cuda.synchronize()
 h = _lib.handle(0)
 h.call("corutv_gemm", 0, m, ell, n, A.data_ptr(), n, X.data_ptr(), ell, C1.data_ptr(), ell)
-h.call("corutv_gemm", 1, n, ell, m, A.data_ptr(), n, Y.data_ptr(), ell, C2.data_ptr(), ell)
+h.call("corutv_gemm", 1, n, ell, m, A.data_ptr(), n, Y.data_ptr(), 112, C2.data_ptr(), ell)
 torch.cuda.synchronize()
 print("ok")
