@@ -56,7 +56,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-rpca", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--e2e-steps", type=int, default=3)
     return p.parse_args()
 
 
