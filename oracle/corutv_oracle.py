@@ -24,13 +24,14 @@ __all__ = [
     "as_matrix", "gaussian_matrix",
     "householder_qr", "qrcp", "jacobi_singular_values", "jacobi_svd",
     "pseudoinverse", "spectral_norm",
-    "corutv", "corutv_lowrank_error", "flop_estimate",
+    "corutv", "corutv_lowrank_error", "flop_estimate", "sor_svd", "tsr_svd", "SECOND_STREAM_OFFSET",
     "shrink", "truncate_utv", "numerical_rank", "next_cap", "alm_corutv",
     "solver_flops",
 ]
 
 VARIANT_EXACT = "exact-d"   # sketch.py:53
 VARIANT_APPROX = "approx-d"  # sketch.py:55
+SECOND_STREAM_OFFSET = 0x9E3779B9  # sketch.py:60 (tsr_svd's second Gaussian stream)
 NNZ_EPS = 1e-12              # rpca.py:44
 RANK_RTOL = 1e-12            # rpca.py:46
 JACOBI_TOL = 1e-14           # dense.py:34
@@ -241,6 +242,8 @@ def _jacobi_tall(a, want_uv):
     u = x[:, order].copy()
     nz = sig > 0.0
     u[:, nz] /= sig[nz]
+    if (~nz).any():
+        _complete_orthonormal(u, np.nonzero(~nz)[0])   # dense.py:347-349
     if q0 is not None:
         u = q0 @ u
     return u, sig, vr[:, order]
@@ -254,9 +257,34 @@ def jacobi_singular_values(a):
     return _jacobi_tall(a, False)[1]
 
 
+def _complete_orthonormal(u, fill):
+    """dense.py:285-310: replace the columns ``fill`` (zero singular values)
+    by unit-vector candidates e_0, e_1, ... Gram-Schmidt'ed (twice) against
+    the kept columns, accepted when their residual norm exceeds 0.1."""
+    m = u.shape[0]
+    keep = [j for j in range(u.shape[1]) if j not in set(int(f) for f in fill)]
+    basis = [u[:, j] for j in keep]
+    cand = 0
+    for j in fill:
+        while True:
+            if cand >= m:
+                raise OracleConvergenceError("orthonormal completion ran out of candidates")
+            w = np.zeros(m)
+            w[cand] = 1.0
+            cand += 1
+            for _ in range(2):
+                for b in basis:
+                    w -= (b @ w) * b
+            nw = np.sqrt((w * w).sum())
+            if nw > 0.1:
+                w /= nw
+                break
+        u[:, j] = w
+        basis.append(w)
+
+
 def jacobi_svd(a):
-    """dense.py:357-376 (no warm start; zero-sigma completion omitted —
-    only reached for exactly rank-deficient inputs the tests avoid)."""
+    """dense.py:357-376 (no warm start).  Returns (u, sigma, v)."""
     a = as_matrix(a, "a")
     if a.shape[0] >= a.shape[1]:
         return _jacobi_tall(a, True)
@@ -340,6 +368,52 @@ def corutv(a, ell, q_power=0, seed=0, variant=VARIANT_EXACT, omega=None,
     if counter is not None:
         counter.passes += passes
     return dict(u=q1 @ qd, t=rd, v=q2[:, perm], perm=perm, passes=passes)
+
+
+def sor_svd(a, ell, q_power=0, seed=0, variant=VARIANT_EXACT, omega=None):
+    """sketch.py:244-262: the corutv pipeline finished by jacobi_svd of the
+    compressed core instead of qrcp.  Returns dict(u, sigma, v, passes)."""
+    a = as_matrix(a, "a")
+    m, n = a.shape
+    if m < n:
+        raise ValueError(f"sor_svd requires rows >= cols, got {m}x{n}")
+    if ell > min(m, n):
+        raise ValueError(f"ell={ell} exceeds min(m, n)={min(m, n)} for a {m}x{n} input")
+    passes = 0
+    c2 = gaussian_matrix(n, ell, seed) if omega is None else np.asarray(omega, float)
+    for _ in range(q_power + 1):
+        c2_in = c2
+        c1 = a @ c2
+        c2 = a.T @ c1
+        passes += 2
+    q1, _ = householder_qr(c1)
+    q2, _ = householder_qr(c2)
+    if variant == VARIANT_EXACT:
+        d = q1.T @ (a @ q2)
+        passes += 1
+    else:
+        d = (q1.T @ c1) @ pseudoinverse(q2.T @ c2_in)
+    fu, fs, fv = jacobi_svd(d)
+    return dict(u=q1 @ fu, sigma=fs, v=q2 @ fv, passes=passes)
+
+
+def tsr_svd(a, ell, seed=0, psi=None, phi=None):
+    """sketch.py:220-241: psi = G(n, ell, seed), phi = G(m, ell, seed +
+    0x9E3779B9 mod 2^64); y = A psi, z = A' phi in one (fused) pass; core =
+    (Q1' y) pinv(Q2' psi); jacobi_svd(core) lifted.  No m >= n requirement."""
+    a = as_matrix(a, "a")
+    m, n = a.shape
+    if ell > min(m, n):
+        raise ValueError(f"ell={ell} exceeds min(m, n)={min(m, n)} for a {m}x{n} input")
+    psi = gaussian_matrix(n, ell, seed) if psi is None else np.asarray(psi, float)
+    phi = (gaussian_matrix(m, ell, (seed + SECOND_STREAM_OFFSET) % 2 ** 64) if phi is None
+           else np.asarray(phi, float))
+    y, z = a @ psi, a.T @ phi
+    q1, _ = householder_qr(y)
+    q2, _ = householder_qr(z)
+    core = (q1.T @ y) @ pseudoinverse(q2.T @ psi)
+    fu, fs, fv = jacobi_svd(core)
+    return dict(u=q1 @ fu, sigma=fs, v=q2 @ fv, passes=1)
 
 
 def corutv_lowrank_error(a, f):

@@ -93,6 +93,31 @@ for name, a, ell, q, seed, variant in cases:
         omega=rsketch.gaussian_matrix(a.shape[1], ell, seed),
         flops=rsketch.flop_estimate(a.shape[0], a.shape[1], ell, q, variant))
 
+# ---- jacobi_svd (dense.py:357), sor_svd / tsr_svd (sketch.py:220-262) ------
+g = np.random.Generator(np.random.PCG64(31))
+for name, a in {
+    "svd_tall": g.standard_normal((15, 9)),
+    "svd_wide": g.standard_normal((7, 12)),
+    "svd_square": g.standard_normal((10, 10)),
+    "svd_zero_cols": np.diag([3.0, 0.0, 2.0, 0.0, 1.0]),          # zero-sigma completion
+}.items():
+    f = rdense.jacobi_svd(a)
+    put(name, "dense.jacobi_svd", a=a, u=f.u, sigma=f.sigma, v=f.v)
+svd_cases = [
+    ("sor_q1", "sor", rank_k(41, 120, 80, 7), 14, 1, 8, "exact-d"),
+    ("sor_q0_approx", "sor", rank_k(42, 90, 60, 5), 10, 0, 3, "approx-d"),
+    ("sor_c2small", "sor", (uu * sig) @ vv.T, 50, 2, 77, "exact-d"),
+    ("tsr_tall", "tsr", rank_k(43, 80, 60, 6), 12, 0, 4, "exact-d"),
+    ("tsr_wide", "tsr", rank_k(44, 50, 90, 5), 10, 0, 6, "exact-d"),
+    ("tsr_noisy", "tsr", rsynth.gen_noisy_lowrank(rsynth.NoisyLowRankSpec(n=100, k=6, seed=22))[0], 20, 0, 1, "exact-d"),
+]
+for name, kind, a, ell, q, seed, variant in svd_cases:
+    cnt = rsketch.PassCounter()
+    cfg = rsketch.SketchConfig(ell=ell, q_power=q, seed=seed, variant=variant)
+    f = (rsketch.sor_svd if kind == "sor" else rsketch.tsr_svd)(a, cfg, cnt)
+    put(name, f"sketch.{kind}_svd(a, SketchConfig(ell={ell}, q_power={q}, seed={seed}, variant={variant!r}))",
+        a=a, u=f.u, sigma=f.sigma, v=f.v, passes=cnt.passes)
+
 # ---- ALM-CoRUTV (rpca.py:237) -------------------------------------------
 def instance(n, seed):  # test_rpca.py:104-108
     k = max(1, round(0.05 * n))

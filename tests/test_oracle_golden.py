@@ -118,3 +118,27 @@ def test_alm_desk_scale_matches_reference(golden):
     assert sol["iterations"] == int(c["iterations"])
     assert sol["ell_history"] == list(c["ell_history"])
     assert np.array_equal(np.flatnonzero(np.abs(sol["s"]) > 1e-12), c["s_support"])
+
+
+@pytest.mark.parametrize("name", ["svd_tall", "svd_wide", "svd_square", "svd_zero_cols"])
+def test_jacobi_svd_matches_reference(golden, name):
+    c = golden[name]
+    u, s, v = O.jacobi_svd(c["a"])
+    assert np.array_equal(s, c["sigma"])
+    assert np.array_equal(u, c["u"]) and np.array_equal(v, c["v"])
+
+
+@pytest.mark.parametrize("name", ["sor_q1", "sor_q0_approx", "sor_c2small", "tsr_tall", "tsr_wide", "tsr_noisy"])
+def test_svd_sketches_match_reference(golden, name):
+    c = golden[name]
+    q, seed = {"sor_q1": (1, 8), "sor_q0_approx": (0, 3), "sor_c2small": (2, 77), "tsr_tall": (0, 4),
+               "tsr_wide": (0, 6), "tsr_noisy": (0, 1)}[name]
+    ell = c["sigma"].size
+    if name.startswith("sor"):
+        variant = O.VARIANT_APPROX if "approx" in name else O.VARIANT_EXACT
+        f = O.sor_svd(c["a"], ell, q, seed, variant)
+    else:
+        f = O.tsr_svd(c["a"], ell, seed)
+    assert f["passes"] == int(c["passes"])
+    assert np.array_equal(f["sigma"], c["sigma"])
+    assert np.array_equal(f["u"], c["u"]) and np.array_equal(f["v"], c["v"])
