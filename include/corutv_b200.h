@@ -103,6 +103,35 @@ int corutv_decompose_host(corutv_handle* h, const double* a_host, int64_t m, int
                           int variant, const double* omega, const uint64_t* pcg_state, double* u,
                           double* t, double* v, int64_t* perm, int64_t* passes_host);
 
+/* Economy SVD by one-sided Jacobi (dense.py:357-376, tol 1e-14, 100
+ * sweeps; zero singular values get the deterministic orthonormal completion
+ * of dense.py:285-310): u (m x k), sigma (k, descending), v (n x k), k =
+ * min(m, n) <= 640, all device row-major.  CORUTV_ERR_CONVERGENCE if the
+ * sweeps do not converge. */
+int corutv_jacobi_svd(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda,
+                      double* u, double* sigma, double* v);
+
+/* sor_svd (sketch.py:244-262): the corutv pipeline (power sketch, both
+ * sketch QRs, exact or approximate compression) finished by a one-sided
+ * Jacobi SVD of the l x l core (dense.py:357-376) instead of the QRCP:
+ * u (m x l) = Q1 Uc, sigma (l, descending), v (n x l) = Q2 Vc, all device.
+ * Omega from `omega` (n x l, device) or, if NULL, from pcg_state.  Requires
+ * m >= n. */
+int corutv_sor_svd(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, int ell,
+                   int q_power, int variant, const double* omega, const uint64_t* pcg_state,
+                   double* u, double* sigma, double* v, int64_t* passes_host);
+
+/* tsr_svd (sketch.py:220-241): two-sided randomized SVD from one
+ * algorithmic pass: y = A psi (psi n x l), z = A' phi (phi m x l), Q1 =
+ * orth(y), Q2 = orth(z), core = (Q1' y) pinv(Q2' psi), Jacobi SVD of the
+ * core, lifted.  psi / phi given (device) or drawn from pcg_psi / pcg_phi
+ * (the reference uses seed and seed + 0x9E3779B9 mod 2^64).  Any m, n with
+ * l <= min(m, n).  *passes_host += 1 (the reference's fused-sweep count). */
+int corutv_tsr_svd(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, int ell,
+                   const double* psi, const uint64_t* pcg_psi, const double* phi,
+                   const uint64_t* pcg_phi, double* u, double* sigma, double* v,
+                   int64_t* passes_host);
+
 /* np.random.Generator(PCG64(seed)).standard_normal((rows, cols)) into out
  * (row-major, ld) on the device, bit-identical (gaussian_matrix,
  * sketch.py:63-68).  Synchronises the stream. */

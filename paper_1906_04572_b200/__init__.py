@@ -27,7 +27,10 @@ from .sketch import (
     count_passes,
     flop_estimate,
     gaussian_matrix,
+    sor_svd,
+    tsr_svd,
 )
+from .dense import SvdFactors
 
 __version__ = "0.1.0"
 
@@ -36,7 +39,7 @@ __all__ = [
     "RpcaSolution", "SketchConfig", "VARIANT_APPROX", "VARIANT_EXACT", "alm_corutv", "corutv",
     "corutv_kpq", "corutv_lowrank_error", "corutv_threshold", "count_passes", "flop_estimate",
     "frobenius_norm", "gaussian_matrix", "install", "shrink", "singular_values", "spectral_norm",
-    "write_telemetry_csv",
+    "write_telemetry_csv", "sor_svd", "tsr_svd", "SvdFactors",
 ]
 
 
@@ -51,6 +54,8 @@ def install(ref_pkg=None):
     done = []
     for modname, name, obj in (
         ("sketch", "corutv", corutv),
+        ("sketch", "sor_svd", sor_svd),
+        ("sketch", "tsr_svd", tsr_svd),
         ("rpca", "corutv", corutv),
         ("bench", "corutv", corutv),
         ("rpca", "alm_corutv", alm_corutv),

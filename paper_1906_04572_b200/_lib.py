@@ -40,6 +40,11 @@ SIGNATURES = {
     "corutv_decompose_seeded": (_I32, [_VP, _VP, _I64, _I64, _I64, _I32, _I32, _I32, _VP, _VP, _VP,
                                        _VP, _VP, c_int64_p]),
     "corutv_gaussian": (_I32, [_VP, _VP, _I64, _I64, _VP, _I64]),
+    "corutv_jacobi_svd": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _VP, _VP]),
+    "corutv_sor_svd": (_I32, [_VP, _VP, _I64, _I64, _I64, _I32, _I32, _I32, _VP, _VP, _VP, _VP, _VP,
+                              c_int64_p]),
+    "corutv_tsr_svd": (_I32, [_VP, _VP, _I64, _I64, _I64, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
+                              c_int64_p]),
     "corutv_decompose_host": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _I64, _I32, _I32, _I32, _VP, _VP,
                                      _VP, _VP, _VP, _VP, c_int64_p]),
     "corutv_decompose_truncated": (_I32, [_VP, _VP, _I64, _I64, _I64, _I32, _I32, _I32, _VP, _VP, _D,

@@ -643,16 +643,17 @@ void qrcp(corutv_handle* h, const double* D, int l, int64_t ldd, double* T, int6
 // one-sided Jacobi: singular values of the matrix whose columns are the nv
 // rows of X (len each); optional pinv.  gwork: (n+1)*(len+n) doubles.
 void jacobi(corutv_handle* h, const double* X, int nv, int len, int64_t ldx, double* sig, double* pinv,
-            int64_t ldp, double* gwork, int* status) {
+            int64_t ldp, double* gwork, int* status, double* ut = nullptr, int64_t ldut = 0,
+            double* vt = nullptr, int64_t ldvt = 0) {
   const int n = nv + (nv > 1 && (nv & 1));
-  const size_t bytes = ((size_t)n * len + (pinv ? (size_t)n * n : 0)) * 8;
+  const size_t bytes = ((size_t)n * len + ((pinv || vt) ? (size_t)n * n : 0)) * 8;
   const int optin = max_optin_smem(h);
   const size_t stat = (small::LMAX * 2) * 8 + 8 * 1024;
   const bool smem = bytes + stat <= (size_t)optin;
   if (smem) set_smem(h, small::jacobi_kernel, bytes);
   const int jt = (int)std::min<int64_t>(1024, std::max<int64_t>(64, 32 * (int64_t)((n + 1) / 2)));
   small::jacobi_kernel<<<1, jt, smem ? bytes : 0, h->stream>>>(
-      X, nv, len, ldx, 1e-14, 100, sig, pinv, ldp, gwork, smem ? 1 : 0, status);
+      X, nv, len, ldx, 1e-14, 100, sig, pinv, ldp, ut, ldut, vt, ldvt, gwork, smem ? 1 : 0, status);
   CK_LAUNCH();
 }
 
@@ -754,6 +755,24 @@ void gaussian(corutv_handle* h, const uint64_t* pcg, int64_t rows, int64_t cols,
 // delta >= 0: ALM truncation (rpca.py:122-132): the QRCP stops at the first
 // |diag T| <= delta (|diag T| is non-increasing), *r_host = that count, and
 // only U[:, :r] / T[:r, :] are formed (V and perm in full).
+// jacobi_svd of the l x l core C (dense.py:357-376), lifted to the sketch
+// bases: u = Q1 Uc (m x l), v = Q2 Vc (n x l), sigma descending.  Work:
+// Xt, UcT, VcT (l x ldp each), gwork (jacobi), jstat (device int).
+void svd_lift(corutv_handle* h, const double* C, int l, int64_t ldp, const double* Q1, int64_t m,
+              const double* Q2, int64_t n, double* Xt, double* UcT, double* VcT, double* gwork, int* jstat,
+              double* u, double* sigma, double* v, double* ws) {
+  transpose(h, C, l, l, ldp, Xt, ldp);  // Jacobi rotates rows = columns of C
+  jacobi(h, Xt, l, l, ldp, sigma, nullptr, 0, gwork, jstat, UcT, ldp, VcT, ldp);
+  run_gemm(h, false, m, l, l, Q1, ldp, UcT, ldp, u, l, nullptr, 0, ws);
+  run_gemm(h, false, n, l, l, Q2, ldp, VcT, ldp, v, l, nullptr, 0, ws);
+  CK(cudaMemcpyAsync(h->pinned, jstat, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  sync(h);
+  int st = 0;
+  std::memcpy(&st, h->pinned, sizeof(int));
+  if (st == 1) fail(h, CORUTV_ERR_CONVERGENCE, "one-sided Jacobi did not converge in 100 sweeps");
+  if (st == 2) fail(h, CORUTV_ERR_CONVERGENCE, "orthonormal completion ran out of candidates");
+}
+
 // Host-resident input (corutv_decompose_host): A is copied into the device
 // buffer `a_dev` (the `a` of decompose) in row chunks on the copy stream, and
 // the first A sweep C1 = A Omega consumes each chunk as soon as it lands, so
@@ -767,8 +786,8 @@ struct HostFeed {
 void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, int ell, int q,
                int variant, const double* omega, const uint64_t* pcg, double* u, double* t, double* v,
                int64_t* perm, int64_t* passes_host, double delta = -1.0, int* r_host = nullptr,
-               const HostFeed* feed = nullptr) {
-  if (!a || (!omega && !pcg) || !u || !t || !v) fail(h, CORUTV_ERR_ARG, "null pointer argument");
+               const HostFeed* feed = nullptr, double* svd_sigma = nullptr) {
+  if (!a || (!omega && !pcg) || !u || (!t && !svd_sigma) || !v) fail(h, CORUTV_ERR_ARG, "null pointer argument");
   if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
   if (ell < 1) fail(h, CORUTV_ERR_ARG, "ell must be >= 1, got " + std::to_string(ell));
   if (ell > small::LMAX) fail(h, CORUTV_ERR_ARG, "ell above the supported maximum 640");
@@ -970,6 +989,13 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
     aux::small_matmul_kernel<<<g, dim3(16, 16), 0, h->stream>>>(B1, ldp, 0, pinvB, ldp, 0, l, l, l, D, ldp);
     CK_LAUNCH();
   }
+  if (svd_sigma) {
+    // sor_svd (sketch.py:244-262): jacobi_svd(D) instead of qrcp, lifted as
+    // U = Q1 Uc, V = Q2 Vc
+    svd_lift(h, D, l, ldp, Q1, m, Q2, n, B2t, qtT, pinvB, gwork, jstat, u, svd_sigma, v, ws);
+    if (passes_host) *passes_host += passes;
+    return;
+  }
   int ucols = l;
   if (delta >= 0.0) {
     qrcp(h, D, l, ldp, t, l, qtT, ldp, reinterpret_cast<long long*>(perm), perm32, gwork, delta, jstat);
@@ -992,6 +1018,104 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   if (passes_host) *passes_host += passes;
 }
 
+
+// ------------------------------------------------------------ tsr_svd
+// Two-sided randomized SVD (sketch.py:220-241): psi (n x l) and phi (m x l)
+// Gaussian (device-drawn from pcg_psi / pcg_phi unless given), y = A psi,
+// z = A' phi, Q1 = orth(y), Q2 = orth(z), core = (Q1' y) pinv(Q2' psi),
+// jacobi_svd(core) lifted.  The two products are one algorithmic pass (the
+// reference's fused_sketch); on the device they are two DMMA sweeps, each
+// FP64-tensor-bound for l >= ~25, so fusing them would not shorten the pass.
+void tsr(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, int ell, const double* psi,
+         const uint64_t* pcg_psi, const double* phi, const uint64_t* pcg_phi, double* u, double* sigma, double* v,
+         int64_t* passes_host) {
+  if (!a || !u || !sigma || !v || (!psi && !pcg_psi) || (!phi && !pcg_phi))
+    fail(h, CORUTV_ERR_ARG, "null pointer argument");
+  if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
+  if (h->world > 1 && h->ar_fn) fail(h, CORUTV_ERR_ARG, "tsr_svd: row-sharded mode is not supported");
+  if (ell < 1) fail(h, CORUTV_ERR_ARG, "ell must be >= 1, got " + std::to_string(ell));
+  if (ell > small::LMAX) fail(h, CORUTV_ERR_ARG, "ell above the supported maximum 640");
+  if ((int64_t)ell > std::min(m, n))
+    fail(h, CORUTV_ERR_SHAPE, "ell=" + std::to_string(ell) + " exceeds min(m, n)=" + std::to_string(std::min(m, n)));
+  if (lda < n) fail(h, CORUTV_ERR_ARG, "lda < n");
+  const int l = ell;
+  const int64_t ldp = round_up(l, 16), ldn = round_up(n, 16);
+  const bool a_ok = ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && (lda % 2 == 0);
+  const int64_t ldA = a_ok ? lda : round_up(n, 16);
+  Arena ar(h);
+  double *Apad = nullptr, *Psi, *PsiT, *Phi, *Y, *Yq, *Yb, *Z, *Zb, *G, *rinvT, *G2, *rinvT2, *gwork, *gwork2;
+  double *ws, *B1, *B2t, *pinvB, *core, *Xt, *UcT, *VcT, *sigs, *flagd;
+  int *flag, *jstat;
+  small::CholInfo* info;
+  if (!a_ok) ar.add(&Apad, (size_t)m * ldA);
+  ar.add(&Psi, (size_t)n * ldp);
+  ar.add(&PsiT, (size_t)l * ldn);
+  ar.add(&Phi, (size_t)m * ldp);
+  ar.add(&Y, (size_t)m * ldp);
+  ar.add(&Yq, (size_t)m * ldp);
+  ar.add(&Yb, (size_t)m * ldp);
+  ar.add(&Z, (size_t)n * ldp);
+  ar.add(&Zb, (size_t)n * ldp);
+  for (double** p : {&G, &rinvT, &G2, &rinvT2, &B1, &B2t, &pinvB, &core, &Xt, &UcT, &VcT}) ar.add(p, (size_t)ldp * ldp);
+  ar.add(&gwork, (size_t)(l + 2) * (2 * l + 4) + 2 * (size_t)l * l + 16);
+  ar.add(&gwork2, (size_t)(l + 2) * (2 * l + 4) + 2 * (size_t)l * l + 16);
+  ar.add(&sigs, (size_t)ldp);
+  ar.add(&flagd, 2);
+  size_t wse = std::max({gemm_ws_elems(h, m, l, n), gemm_ws_elems(h, n, l, m), gemm_ws_elems(h, l, l, m),
+                         gemm_ws_elems(h, l, l, n)});
+  ar.add(&ws, wse + 16);
+  ar.add(&flag, 4);
+  ar.add(&jstat, 4);
+  ar.add(&info, 4);
+  ar.commit();
+  const double* A = a;
+  if (!a_ok) {
+    copy2d(h, a, m, n, lda, Apad, ldA);
+    A = Apad;
+  }
+  CK(cudaMemsetAsync(flag, 0, sizeof(int), h->stream));
+  if (psi) {
+    copy2d(h, psi, n, l, l, Psi, ldp);
+    transpose(h, psi, n, l, l, PsiT, ldn);
+  } else {
+    gaussian(h, pcg_psi, n, l, Psi, ldp, PsiT, ldn);
+  }
+  if (phi) copy2d(h, phi, m, l, l, Phi, ldp);
+  else gaussian(h, pcg_phi, m, l, Phi, ldp, nullptr, 0);
+  {
+    TagScope ts(h, 1);
+    run_gemm(h, false, m, l, n, A, ldA, PsiT, ldn, Y, ldp, nullptr, 0, ws, flag);  // y = A psi
+    run_gemm(h, true, n, l, m, A, ldA, Phi, ldp, Z, ldp, nullptr, 0, ws);          // z = A' phi
+  }
+  aux::flag_to_double_kernel<<<1, 32, 0, h->stream>>>(flag, flagd);
+  CK_LAUNCH();
+  CK(cudaMemcpyAsync(Yq, Y, (size_t)m * ldp * 8, cudaMemcpyDeviceToDevice, h->stream));
+  QrJob jobs[2];
+  jobs[0].cur = Yq;
+  jobs[0].nxt = Yb;
+  jobs[0].rows = m;
+  jobs[0].rows_global = (double)m;
+  jobs[0].sharded = false;
+  jobs[0].w = QrWork{G, rinvT, gwork, ws, info};
+  jobs[1].cur = Z;
+  jobs[1].nxt = Zb;
+  jobs[1].rows = n;
+  jobs[1].rows_global = (double)n;
+  jobs[1].sharded = false;
+  jobs[1].w = QrWork{G2, rinvT2, gwork2, ws, info + 2};
+  cholqr_multi(h, jobs, 2, l, ldp, flagd);
+  const double* Q1 = jobs[0].cur;
+  const double* Q2 = jobs[1].cur;
+  // core = (Q1' y) pinv(Q2' psi)   (sketch.py:239, dense.py:390-402)
+  run_gemm(h, true, l, l, m, Q1, ldp, Y, ldp, B1, ldp, nullptr, 0, ws);     // B1 = Q1' y
+  run_gemm(h, true, l, l, n, Psi, ldp, Q2, ldp, B2t, ldp, nullptr, 0, ws);  // B2' = psi' Q2
+  jacobi(h, B2t, l, l, ldp, sigs, pinvB, ldp, gwork, jstat);                // pinv(B2)
+  dim3 g((l + 15) / 16, (l + 15) / 16);
+  aux::small_matmul_kernel<<<g, dim3(16, 16), 0, h->stream>>>(B1, ldp, 0, pinvB, ldp, 0, l, l, l, core, ldp);
+  CK_LAUNCH();
+  svd_lift(h, core, l, ldp, Q1, m, Q2, n, Xt, UcT, VcT, gwork, jstat, u, sigma, v, ws);
+  if (passes_host) *passes_host += 1;
+}
 
 // --------------------------------------------- low-rank product epilogues
 template <int J, int MODE>
@@ -1338,6 +1462,71 @@ int corutv_decompose_host(corutv_handle* hh, const double* a_host, int64_t m, in
   HostFeed feed{a_host, lda_host, a_dev};
   decompose(h, a_dev, m, n, ld_dev, ell, q_power, variant, omega, omega ? nullptr : st, u, t, v, perm,
             passes_host, -1.0, nullptr, &feed);
+  ABI_END
+}
+
+int corutv_jacobi_svd(corutv_handle* hh, const double* a, int64_t m, int64_t n, int64_t lda, double* u,
+                      double* sigma, double* v) {
+  ABI_BEGIN(hh)
+  if (!a || !u || !sigma || !v) fail(h, CORUTV_ERR_ARG, "null pointer argument");
+  if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
+  const int64_t k = std::min(m, n), len = std::max(m, n);
+  if (k > small::LMAX) fail(h, CORUTV_ERR_ARG, "jacobi_svd: min(m, n) above the supported maximum 640");
+  const int64_t ldl = round_up(len, 2), ldk = round_up(k, 2);
+  Arena ar(h);
+  double *X, *UT, *VT, *gw;
+  int* st;
+  ar.add(&X, (size_t)k * ldl);
+  ar.add(&UT, (size_t)k * ldl);
+  ar.add(&VT, (size_t)k * ldk);
+  ar.add(&gw, (size_t)(k + 2) * (len + k + 2) + 16);
+  ar.add(&st, 4);
+  ar.commit();
+  // rotate the columns of the tall orientation (dense.py:371-376)
+  if (m >= n) transpose(h, a, m, n, lda, X, ldl);
+  else copy2d(h, a, m, n, lda, X, ldl);
+  jacobi(h, X, (int)k, (int)len, ldl, sigma, nullptr, 0, gw, st, UT, ldl, VT, ldk);
+  if (m >= n) {
+    transpose(h, UT, k, m, ldl, u, k);   // u = UT'  (m x k)
+    transpose(h, VT, k, n, ldk, v, k);   // v = VT'  (n x n)
+  } else {
+    transpose(h, VT, k, m, ldk, u, k);   // wide: factors of A' swapped
+    transpose(h, UT, k, n, ldl, v, k);
+  }
+  CK(cudaMemcpyAsync(h->pinned, st, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  sync(h);
+  int s0 = 0;
+  std::memcpy(&s0, h->pinned, sizeof(int));
+  if (s0 == 1) fail(h, CORUTV_ERR_CONVERGENCE, "one-sided Jacobi did not converge in 100 sweeps");
+  if (s0 == 2) fail(h, CORUTV_ERR_CONVERGENCE, "orthonormal completion ran out of candidates");
+  ABI_END
+}
+
+int corutv_sor_svd(corutv_handle* hh, const double* a, int64_t m, int64_t n, int64_t lda, int ell, int q_power,
+                   int variant, const double* omega, const uint64_t* pcg_state, double* u, double* sigma, double* v,
+                   int64_t* passes_host) {
+  ABI_BEGIN(hh)
+  if (!sigma) fail(h, CORUTV_ERR_ARG, "null pointer argument");
+  uint64_t st[4] = {0, 0, 0, 0};
+  if (!omega) {
+    if (!pcg_state) fail(h, CORUTV_ERR_ARG, "need omega or pcg_state");
+    for (int i = 0; i < 4; ++i) st[i] = pcg_state[i];
+  }
+  decompose(h, a, m, n, lda, ell, q_power, variant, omega, omega ? nullptr : st, u, nullptr, v, nullptr,
+            passes_host, -1.0, nullptr, nullptr, sigma);
+  ABI_END
+}
+
+int corutv_tsr_svd(corutv_handle* hh, const double* a, int64_t m, int64_t n, int64_t lda, int ell,
+                   const double* psi, const uint64_t* pcg_psi, const double* phi, const uint64_t* pcg_phi, double* u,
+                   double* sigma, double* v, int64_t* passes_host) {
+  ABI_BEGIN(hh)
+  uint64_t s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0};
+  if (pcg_psi)
+    for (int i = 0; i < 4; ++i) s1[i] = pcg_psi[i];
+  if (pcg_phi)
+    for (int i = 0; i < 4; ++i) s2[i] = pcg_phi[i];
+  tsr(h, a, m, n, lda, ell, psi, pcg_psi ? s1 : nullptr, phi, pcg_phi ? s2 : nullptr, u, sigma, v, passes_host);
   ABI_END
 }
 

@@ -518,8 +518,9 @@ __global__ void __launch_bounds__(1024, 1)
 // max(len, nv) * sig0 * 1e-12 (dense.py:390-402).
 __global__ void __launch_bounds__(THREADS, 1)
     jacobi_kernel(const double* __restrict__ X, int nv, int len, int64_t ldx, double tol,
-                  int max_sweeps, double* sig_out, double* pinv, int64_t ldp, double* gwork,
-                  int use_smem, int* status) {
+                  int max_sweeps, double* sig_out, double* pinv, int64_t ldp, double* ut_out,
+                  int64_t ldut, double* vt_out, int64_t ldvt, double* gwork, int use_smem,
+                  int* status) {
   extern __shared__ double dsm[];
   __shared__ double offmax[NWARPS];
   __shared__ double sig[LMAX];
@@ -528,7 +529,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int nwarps = blockDim.x >> 5;
   const int nt = blockDim.x;
   const int n = nv + (nv > 1 && (nv & 1));  // pad odd counts with a zero row
-  const bool want_v = pinv != nullptr;
+  const bool want_v = pinv != nullptr || vt_out != nullptr;
   double* W = use_smem ? dsm : gwork;          // n x len
   double* V = W + (int64_t)n * len;            // n x n (row a = column a of V)
   for (int r = warp; r < n; r += nwarps)
@@ -615,7 +616,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   __syncthreads();
   for (int k = threadIdx.x; k < nv; k += nt) sig_out[k] = sig[order[k]];
-  if (want_v) {
+  if (pinv) {
     // B = X^T = U S V^T with U[:, k] = W[k] / sig_k.  pinv = V S^+ U^T.
     const double s0 = sig[order[0]];
     const double cut = (double)max(len, nv) * s0 * 1e-12;
@@ -630,6 +631,61 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         pinv[i * ldp + j] = acc;
       }
+  }
+  if (ut_out || vt_out) {
+    // economy SVD of B = X^T (dense.py:339-352): B[:, order[k]] / sig_k is
+    // left vector k (row k of ut_out), column order[k] of the accumulated
+    // rotations right vector k (row k of vt_out)
+    for (int k = warp; k < nv; k += nwarps) {
+      const int r = order[k];
+      const double sk = sig[r];
+      if (ut_out)
+        for (int i = lane; i < len; i += 32)
+          ut_out[k * ldut + i] = (sk > 0.0) ? W[(int64_t)r * len + i] / sk : 0.0;
+      if (vt_out)
+        for (int i = lane; i < nv; i += 32) vt_out[k * ldvt + i] = V[(int64_t)r * n + i];
+    }
+    __syncthreads();
+    // zero singular values: complete the left factor (dense.py:285-310)
+    // with unit-vector candidates, Gram-Schmidt'ed twice against the kept
+    // vectors in index order, accepted above norm 0.1
+    if (ut_out && warp == 0) {
+      int cand = 0;
+      for (int j = 0; j < nv; ++j) {
+        if (sig[order[j]] > 0.0) continue;
+        for (;;) {
+          if (cand >= len) {
+            st = 2;
+            break;
+          }
+          for (int i = lane; i < len; i += 32) ut_out[j * ldut + i] = (i == cand) ? 1.0 : 0.0;
+          ++cand;
+          __syncwarp();
+          for (int pass = 0; pass < 2; ++pass) {
+            // basis: kept vectors (sig > 0) in index order, then earlier fills
+            for (int b = 0; b < 2 * nv; ++b) {
+              const int kb = b < nv ? b : b - nv;
+              const bool kept = sig[order[kb]] > 0.0;
+              if (b < nv ? !kept : (kept || kb >= j)) continue;
+              double d = 0.0;
+              for (int i = lane; i < len; i += 32) d += ut_out[kb * ldut + i] * ut_out[j * ldut + i];
+              d = warp_sum(d);
+              for (int i = lane; i < len; i += 32) ut_out[j * ldut + i] -= d * ut_out[kb * ldut + i];
+              __syncwarp();
+            }
+          }
+          double nw = 0.0;
+          for (int i = lane; i < len; i += 32) nw += ut_out[j * ldut + i] * ut_out[j * ldut + i];
+          nw = sqrt(warp_sum(nw));
+          if (nw > 0.1) {
+            for (int i = lane; i < len; i += 32) ut_out[j * ldut + i] /= nw;
+            __syncwarp();
+            break;
+          }
+        }
+        if (st == 2) break;
+      }
+    }
   }
   if (threadIdx.x == 0 && status) *status = st;
 }

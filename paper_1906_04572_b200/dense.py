@@ -10,11 +10,23 @@ from __future__ import annotations
 
 import ctypes
 import math
+from dataclasses import dataclass
 
 from . import _device as dev
 from . import _lib
 
-__all__ = ["spectral_norm", "singular_values", "frobenius_norm", "spectral_norm_iters"]
+__all__ = ["spectral_norm", "singular_values", "frobenius_norm", "spectral_norm_iters", "SvdFactors",
+           "jacobi_svd"]
+
+
+@dataclass
+class SvdFactors:
+    """dense.py:71-78: economy SVD factors, ``u * sigma @ v.T`` reconstructs
+    the input; sigma non-negative and non-increasing."""
+
+    u: object
+    sigma: object
+    v: object
 
 
 def spectral_norm_iters(a, tol: float = 1e-10, max_iter: int = 5000):
@@ -63,3 +75,19 @@ def frobenius_norm(a) -> float:
     if not math.isfinite(out.value):
         dev.raise_if_nonfinite(A, "a")
     return math.sqrt(out.value)
+
+
+def jacobi_svd(a) -> SvdFactors:
+    """dense.py:357-376 (no warm start) on the device: economy SVD of a
+    matrix with min(m, n) <= 640 (corutv_jacobi_svd)."""
+    torch = dev.torch_mod()
+    A, was_host = dev.to_device(a, "a")
+    dev.raise_if_nonfinite(A, "a")
+    m, n = A.shape
+    k = min(m, n)
+    u = torch.empty((m, k), dtype=torch.float64, device=A.device)
+    s = torch.empty((k,), dtype=torch.float64, device=A.device)
+    v = torch.empty((n, k), dtype=torch.float64, device=A.device)
+    h = _lib.handle(A.device.index)
+    h.call("corutv_jacobi_svd", dev.ptr(A), m, n, A.stride(0), dev.ptr(u), dev.ptr(s), dev.ptr(v))
+    return SvdFactors(u=dev.to_output(u, was_host), sigma=dev.to_output(s, was_host), v=dev.to_output(v, was_host))

@@ -19,6 +19,7 @@ import numpy as np
 
 from . import _device as dev
 from . import _lib
+from .dense import SvdFactors
 
 __all__ = [
     "VARIANT_EXACT",
@@ -32,7 +33,12 @@ __all__ = [
     "corutv_lowrank_error",
     "count_passes",
     "flop_estimate",
+    "sor_svd",
+    "tsr_svd",
+    "SvdFactors",
 ]
+
+SECOND_STREAM_OFFSET = 0x9E3779B9  # sketch.py:60
 
 VARIANT_EXACT = "exact-d"   # sketch.py:53
 VARIANT_APPROX = "approx-d"  # sketch.py:55
@@ -265,6 +271,64 @@ def corutv_truncated(A, cfg: SketchConfig, delta: float, counter: PassCounter | 
         counter.add(passes.value)
     return CorUtvFactors(u=u, t=t, v=v, ell=ell, q_power=cfg.q_power, variant=cfg.variant,
                          perm=perm), int(r.value)
+
+
+def _svd_outputs(u, sigma, v, was_host):
+    return SvdFactors(u=dev.to_output(u, was_host), sigma=dev.to_output(sigma, was_host),
+                      v=dev.to_output(v, was_host))
+
+
+def sor_svd(a, cfg: SketchConfig, counter: PassCounter | None = None, omega=None) -> SvdFactors:
+    """sketch.py:244-262: the corutv pipeline finished by a Jacobi SVD of the
+    compressed core (corutv_sor_svd)."""
+    torch = dev.torch_mod()
+    A, was_host = dev.to_device(a, "a")
+    dev.raise_if_nonfinite(A, "a")
+    m, n = A.shape
+    if m < n:
+        raise ValueError(f"sor_svd requires rows >= cols, got {m}x{n}")
+    cfg.validated_for(m, n)
+    ell = cfg.ell
+    u = torch.empty((m, ell), dtype=torch.float64, device=A.device)
+    s = torch.empty((ell,), dtype=torch.float64, device=A.device)
+    v = torch.empty((n, ell), dtype=torch.float64, device=A.device)
+    om = None if omega is None else _omega_device(omega, n, ell, cfg.seed, A)
+    passes = ctypes.c_int64(0)
+    h = _lib.handle(A.device.index)
+    h.call("corutv_sor_svd", dev.ptr(A), m, n, A.stride(0), ell, cfg.q_power, _VARIANT_CODE[cfg.variant],
+           None if om is None else dev.ptr(om), None if om is not None else pcg_state(cfg.seed),
+           dev.ptr(u), dev.ptr(s), dev.ptr(v), ctypes.byref(passes))
+    if counter is not None:
+        counter.add(passes.value)
+    return _svd_outputs(u, s, v, was_host)
+
+
+def tsr_svd(a, cfg: SketchConfig, counter: PassCounter | None = None, psi=None, phi=None) -> SvdFactors:
+    """sketch.py:220-241: two-sided randomized SVD, psi = G(n, ell, seed),
+    phi = G(m, ell, seed + 0x9E3779B9 mod 2^64) drawn on the device
+    (corutv_tsr_svd).  One algorithmic pass (counted as the reference's
+    fused sweep)."""
+    torch = dev.torch_mod()
+    A, was_host = dev.to_device(a, "a")
+    dev.raise_if_nonfinite(A, "a")
+    m, n = A.shape
+    cfg.validated_for(m, n)
+    ell = cfg.ell
+    u = torch.empty((m, ell), dtype=torch.float64, device=A.device)
+    s = torch.empty((ell,), dtype=torch.float64, device=A.device)
+    v = torch.empty((n, ell), dtype=torch.float64, device=A.device)
+    ps = None if psi is None else _omega_device(psi, n, ell, cfg.seed, A)
+    ph = None if phi is None else _omega_device(phi, m, ell, cfg.seed, A)
+    passes = ctypes.c_int64(0)
+    h = _lib.handle(A.device.index)
+    h.call("corutv_tsr_svd", dev.ptr(A), m, n, A.stride(0), ell,
+           None if ps is None else dev.ptr(ps), None if ps is not None else pcg_state(cfg.seed),
+           None if ph is None else dev.ptr(ph),
+           None if ph is not None else pcg_state((cfg.seed + SECOND_STREAM_OFFSET) % 2 ** 64),
+           dev.ptr(u), dev.ptr(s), dev.ptr(v), ctypes.byref(passes))
+    if counter is not None:
+        counter.add(passes.value)
+    return _svd_outputs(u, s, v, was_host)
 
 
 def corutv_kpq(a, k: int, p: int, q: int, omega=None, seed: int = 0,
