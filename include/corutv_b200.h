@@ -30,8 +30,14 @@ enum corutv_status {
   CORUTV_ERR_COMM = 4,       /* collective failure in the row-sharded path (CorutvError) */
   CORUTV_ERR_CONVERGENCE = 5,/* iteration cap hit (ConvergenceError, errors.py:8-18) */
   CORUTV_ERR_ARG = 6,        /* invalid argument (ValueError) */
-  CORUTV_ERR_NOMEM = 7       /* device allocation failed (CorutvError) */
+  CORUTV_ERR_NOMEM = 7,      /* device allocation failed (CorutvError) */
+  CORUTV_ERR_IO = 8          /* the row-reader callback failed (OSError) */
 };
+
+/* Row reader for streamed input: fill dst (rows x n, leading dimension ld,
+ * pinned host memory owned by the library) with rows [row0, row0 + rows)
+ * of the matrix; return 0 on success. */
+typedef int (*corutv_read_rows_fn)(void* user, int64_t row0, int64_t rows, double* dst, int64_t ld);
 
 enum corutv_variant { CORUTV_EXACT_D = 0, CORUTV_APPROX_D = 1 }; /* sketch.py:52-55 */
 
@@ -131,6 +137,18 @@ int corutv_tsr_svd(corutv_handle* h, const double* a, int64_t m, int64_t n, int6
                    const double* psi, const uint64_t* pcg_psi, const double* phi,
                    const uint64_t* pcg_phi, double* u, double* sigma, double* v,
                    int64_t* passes_host);
+
+/* corutv of a matrix that is never resident in host memory (an out-of-core
+ * file): the library pulls ~1 GiB row chunks through
+ * read_rows into two pinned staging buffers, copies each to the caller's
+ * device buffer a_dev (m x ld_dev, 16-byte aligned, ld_dev even) on a copy
+ * stream and runs the first sketch sweeps on each chunk as it lands, as
+ * corutv_decompose_host does; the read of chunk c+1 overlaps the copy and
+ * the sweeps of chunk c.  Bit-identical to corutv_decompose on a_dev. */
+int corutv_decompose_stream(corutv_handle* h, corutv_read_rows_fn read_rows, void* user, int64_t m,
+                            int64_t n, double* a_dev, int64_t ld_dev, int ell, int q_power,
+                            int variant, const double* omega, const uint64_t* pcg_state,
+                            double* u, double* t, double* v, int64_t* perm, int64_t* passes_host);
 
 /* np.random.Generator(PCG64(seed)).standard_normal((rows, cols)) into out
  * (row-major, ld) on the device, bit-identical (gaussian_matrix,

@@ -18,13 +18,15 @@ from .errors import ConvergenceError, CorutvError
 LIB_NAME = "libcorutv_b200.so"
 LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
 
-OK, ERR_SHAPE, ERR_NONFINITE, ERR_CUDA, ERR_COMM, ERR_CONVERGENCE, ERR_ARG, ERR_NOMEM = range(8)
+OK, ERR_SHAPE, ERR_NONFINITE, ERR_CUDA, ERR_COMM, ERR_CONVERGENCE, ERR_ARG, ERR_NOMEM, ERR_IO = range(9)
 EXACT_D, APPROX_D = 0, 1
 
 c_double_p = ctypes.POINTER(ctypes.c_double)
 c_int64_p = ctypes.POINTER(ctypes.c_int64)
 ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                 ctypes.c_void_p)
+READ_ROWS_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                ctypes.c_void_p, ctypes.c_int64)
 
 # name -> (restype, argtypes); mirrors include/corutv_b200.h
 _VP, _I64, _I32, _D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
@@ -40,6 +42,8 @@ SIGNATURES = {
     "corutv_decompose_seeded": (_I32, [_VP, _VP, _I64, _I64, _I64, _I32, _I32, _I32, _VP, _VP, _VP,
                                        _VP, _VP, c_int64_p]),
     "corutv_gaussian": (_I32, [_VP, _VP, _I64, _I64, _VP, _I64]),
+    "corutv_decompose_stream": (_I32, [_VP, READ_ROWS_FN, _VP, _I64, _I64, _VP, _I64, _I32, _I32, _I32, _VP,
+                                       _VP, _VP, _VP, _VP, _VP, c_int64_p]),
     "corutv_jacobi_svd": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _VP, _VP]),
     "corutv_sor_svd": (_I32, [_VP, _VP, _I64, _I64, _I64, _I32, _I32, _I32, _VP, _VP, _VP, _VP, _VP,
                               c_int64_p]),
@@ -104,6 +108,8 @@ def check(status: int, handle=None, what: str = "") -> None:
         raise ValueError(msg or text)
     if status == ERR_CONVERGENCE:
         raise ConvergenceError(text)
+    if status == ERR_IO:
+        raise OSError(text)
     raise CorutvError(f"{text} (status {status})")
 
 

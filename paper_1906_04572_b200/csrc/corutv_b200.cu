@@ -49,6 +49,8 @@ struct corutv_handle {
   // one event per row chunk
   cudaStream_t copy_stream = nullptr;
   std::vector<cudaEvent_t> chunk_ev;
+  double* staging = nullptr;  // 2 pinned row-chunk buffers (corutv_decompose_stream)
+  size_t staging_bytes = 0;   // per buffer
   // profiling (corutv_profile_begin/end): launch counter always on; CUDA
   // events around the DMMA GEMM / low-rank kernels while enabled.
   int64_t launches = 0;
@@ -778,9 +780,11 @@ void svd_lift(corutv_handle* h, const double* C, int l, int64_t ldp, const doubl
 // the first A sweep C1 = A Omega consumes each chunk as soon as it lands, so
 // the H2D transfer overlaps the generation of Omega and the first sweep.
 struct HostFeed {
-  const double* a_host;
+  const double* a_host;      // resident host matrix, or
   int64_t ld_host;
   double* a_dev;
+  corutv_read_rows_fn read_rows = nullptr;  // rows pulled into pinned staging
+  void* user = nullptr;
 };
 
 void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, int ell, int q,
@@ -854,9 +858,19 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   int64_t chunk_rows = 0, n_chunks = 0;
   auto enqueue_chunk = [&](int64_t c) {
     const int64_t r0 = c * chunk_rows, rows = std::min(chunk_rows, m - r0);
-    CK(cudaMemcpy2DAsync(feed->a_dev + r0 * lda, (size_t)lda * 8, feed->a_host + r0 * feed->ld_host,
-                         (size_t)feed->ld_host * 8, (size_t)n * 8, (size_t)rows, cudaMemcpyHostToDevice,
-                         h->copy_stream));
+    const double* src = feed->a_host + r0 * feed->ld_host;
+    int64_t ld_src = feed->ld_host;
+    if (feed->read_rows) {
+      // staging slot c % 2 was last used by chunk c - 2: wait for its copy
+      double* slot = h->staging + (size_t)(c & 1) * (h->staging_bytes / 8);
+      if (c >= 2) CK(cudaEventSynchronize(h->chunk_ev[c - 2]));
+      if (feed->read_rows(feed->user, r0, rows, slot, n) != 0)
+        fail(h, CORUTV_ERR_IO, "row reader failed at rows " + std::to_string(r0) + ".." + std::to_string(r0 + rows));
+      src = slot;
+      ld_src = n;
+    }
+    CK(cudaMemcpy2DAsync(feed->a_dev + r0 * lda, (size_t)lda * 8, src, (size_t)ld_src * 8, (size_t)n * 8,
+                         (size_t)rows, cudaMemcpyHostToDevice, h->copy_stream));
     CK(cudaEventRecord(h->chunk_ev[c], h->copy_stream));
   };
   if (feed) {
@@ -869,6 +883,19 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
     chunk_rows = std::max<int64_t>(gemm::BM, chunk_bytes / (8 * n) / gemm::BM * gemm::BM);
     chunk_rows = std::min(chunk_rows, m);
     n_chunks = (m + chunk_rows - 1) / chunk_rows;
+    if (feed->read_rows) {
+      const size_t need = (size_t)chunk_rows * n * 8;
+      if (h->staging_bytes < need) {
+        if (h->staging) CK(cudaFreeHost(h->staging));
+        h->staging = nullptr;
+        h->staging_bytes = 0;
+        if (cudaMallocHost(&h->staging, 2 * need) != cudaSuccess) {
+          cudaGetLastError();
+          fail(h, CORUTV_ERR_NOMEM, "pinned staging allocation failed");
+        }
+        h->staging_bytes = need;
+      }
+    }
     while ((int64_t)h->chunk_ev.size() < n_chunks) {
       cudaEvent_t e;
       CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1391,6 +1418,7 @@ void corutv_destroy(corutv_handle* h) {
   if (h->arena) cudaFree(h->arena);
   if (h->pinned) cudaFreeHost(h->pinned);
   for (cudaEvent_t e : h->chunk_ev) cudaEventDestroy(e);
+  if (h->staging) cudaFreeHost(h->staging);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   delete h;
 }
@@ -1527,6 +1555,25 @@ int corutv_tsr_svd(corutv_handle* hh, const double* a, int64_t m, int64_t n, int
   if (pcg_phi)
     for (int i = 0; i < 4; ++i) s2[i] = pcg_phi[i];
   tsr(h, a, m, n, lda, ell, psi, pcg_psi ? s1 : nullptr, phi, pcg_phi ? s2 : nullptr, u, sigma, v, passes_host);
+  ABI_END
+}
+
+int corutv_decompose_stream(corutv_handle* hh, corutv_read_rows_fn read_rows, void* user, int64_t m, int64_t n,
+                            double* a_dev, int64_t ld_dev, int ell, int q_power, int variant, const double* omega,
+                            const uint64_t* pcg_state, double* u, double* t, double* v, int64_t* perm,
+                            int64_t* passes_host) {
+  ABI_BEGIN(hh)
+  if (!read_rows || !a_dev) fail(h, CORUTV_ERR_ARG, "null pointer argument");
+  if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
+  if (ld_dev < n) fail(h, CORUTV_ERR_ARG, "leading dimension < n");
+  uint64_t st[4] = {0, 0, 0, 0};
+  if (!omega) {
+    if (!pcg_state) fail(h, CORUTV_ERR_ARG, "need omega or pcg_state");
+    for (int i = 0; i < 4; ++i) st[i] = pcg_state[i];
+  }
+  HostFeed feed{nullptr, 0, a_dev, read_rows, user};
+  decompose(h, a_dev, m, n, ld_dev, ell, q_power, variant, omega, omega ? nullptr : st, u, t, v, perm,
+            passes_host, -1.0, nullptr, &feed);
   ABI_END
 }
 

@@ -528,3 +528,39 @@ def test_alm_update_matches_torch_formula():
     assert float((G - ((M - s_ref) + y_ref / mu_next)).abs().max()) < 1e-12
     assert abs(z2.value - float((z * z).sum())) <= 1e-12 * float((z * z).sum())
     assert nnz.value == int((s_ref.abs() > 1e-12).sum())
+
+
+@pytest.mark.parametrize("chunk_bytes", [None, 1 << 20])
+def test_corutv_file_streams_bitwise(tmp_path, monkeypatch, chunk_bytes):
+    """corutv of a CRUTVMAT file streamed disk -> pinned staging
+    -> device equals corutv of the same matrix in memory, bit for bit."""
+    from paper_1906_04572_b200 import matio
+
+    if chunk_bytes is not None:
+        monkeypatch.setenv("CORUTV_HOST_CHUNK_BYTES", str(chunk_bytes))
+    rng = np.random.Generator(np.random.PCG64(12))
+    a = rng.standard_normal((3000, 20)) @ rng.standard_normal((20, 450)) + 1e-4 * rng.standard_normal((3000, 450))
+    p = tmp_path / "a.bin"
+    matio.write_matrix_bin(p, a)
+    cfg = P.SketchConfig(ell=25, q_power=2, seed=4)
+    cnt = P.PassCounter()
+    f = matio.corutv_file(p, cfg, cnt)
+    g = P.corutv(torch.from_numpy(a).cuda(), cfg)
+    assert cnt.passes == 7
+    for x, y in ((f.u, g.u), (f.t, g.t), (f.v, g.v), (f.perm, g.perm)):
+        assert np.array_equal(x, y.cpu().numpy())
+
+
+def test_corutv_file_errors(tmp_path):
+    from paper_1906_04572_b200 import matio
+
+    rng = np.random.Generator(np.random.PCG64(13))
+    a = rng.standard_normal((600, 100))
+    a[555, 3] = np.nan
+    p = tmp_path / "nan.bin"
+    matio.write_matrix_bin(p, a)
+    with pytest.raises(ValueError, match="non-finite"):
+        matio.corutv_file(p, P.SketchConfig(ell=5))
+    matio.write_matrix_bin(p, rng.standard_normal((50, 80)))
+    with pytest.raises(ValueError, match="rows >= cols"):
+        matio.corutv_file(p, P.SketchConfig(ell=5))
