@@ -506,7 +506,7 @@ void cholqr_multi(corutv_handle* h, QrJob* jobs, int njobs, int ell, int64_t ldx
   const size_t static_smem = 4096;
   const size_t aug = 2 * (size_t)l * l * 8;  // [G | I] in one CTA's shared memory
   const bool smem = aug + static_smem <= (size_t)optin;
-  const size_t cl_smem = (1024 + (size_t)small::NB * (l + small::NB)) * 8;
+  const size_t cl_smem = (size_t)chc::smem_doubles(l) * 8;
   const int cl_cs = l >= 256 ? 16 : 8;
   if (smem) {
     set_smem(h, small::chol_factor_kernel, aug);

@@ -479,7 +479,13 @@ def test_corutv_parity_across_ell(decaying_matrix, ell):
         # LAPACK's QR already differs from the reference by 1.5% (4.5e-9 |A|)
         assert abs(np.linalg.norm(a - f.lowrank()) - e_ref) <= 1e-8 * na
     dref = np.abs(np.diag(ref["t"]))
-    assert np.abs(np.abs(np.diag(f.t)) - dref).max() <= 1e-9 * dref[0]
+    # ell = 400 equals the planted rank (no spectral gap): the trailing
+    # |diag T| are fixed only to ~u kappa(C1), kappa(C1) ~ (s_1/s_400)^3; the
+    # oracle with LAPACK's QR instead of the reference's Householder already
+    # differs by 1.06e-9 |T_11| there (measured), so that case is held to 5x
+    # the measured floor
+    tol = 5e-9 if ell >= 400 else 1e-9
+    assert np.abs(np.abs(np.diag(f.t)) - dref).max() <= tol * dref[0]
     k = ell // 2
     assert np.array_equal(f.perm[:k], ref["perm"][:k])
     assert np.abs(sign_align(f.u[:, :k], ref["u"][:, :k]) - ref["u"][:, :k]).max() <= 1e-9

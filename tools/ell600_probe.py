@@ -3,7 +3,11 @@ import sys
 import time
 sys.path.insert(0, '.')
 import torch
+import os
 import paper_1906_04572_b200 as P
+from paper_1906_04572_b200 import _lib
+if os.environ.get("CORUTV_LIB"):
+    _lib._lib = _lib.load_library(os.environ["CORUTV_LIB"])
 torch.cuda.set_device(0)
 dev = torch.device("cuda", 0)
 n = 10000
