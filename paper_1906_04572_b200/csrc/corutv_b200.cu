@@ -505,7 +505,10 @@ void cholqr_multi(corutv_handle* h, QrJob* jobs, int njobs, int ell, int64_t ldx
   const int optin = max_optin_smem(h);
   const size_t static_smem = 4096;
   const size_t aug = 2 * (size_t)l * l * 8;  // [G | I] in one CTA's shared memory
-  const bool smem = aug + static_smem <= (size_t)optin;
+  // one-CTA kernel for small cores; the cluster kernel (lookahead, DMMA
+  // updates) wins from l ~ 64 on (C2 l = 50: equal, C3 l = 110: -0.8 ms/step)
+  static const bool force_cluster = std::getenv("CORUTV_CHOL_CLUSTER") != nullptr;  // tuning knob
+  const bool smem = aug + static_smem <= (size_t)optin && l < 64 && !force_cluster;
   const size_t cl_smem = (size_t)chc::smem_doubles(l) * 8;
   const int cl_cs = l >= 256 ? 16 : 8;
   if (smem) {
