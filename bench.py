@@ -242,10 +242,27 @@ def ncu_traffic(wl):
 
 
 # ---------------------------------------------------------------- reference arm
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def all_blas_threads():
+    """BLAS thread pool sized to every usable host core (torchrun exports
+    OMP_NUM_THREADS=1 to each rank, which would starve the CPU arm)."""
+    from threadpoolctl import threadpool_limits
+
+    return threadpool_limits(limits=host_cores(), user_api="blas")
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return 0
     import oracle as O
+
+    _pool = all_blas_threads()  # noqa: F841  (held for the run)
 
     wl = args.workload
     m, n, ell, q, *_ = WORKLOADS[wl]
@@ -261,7 +278,7 @@ def run_reference(args, world, rank):
     t = float(np.mean(times))
     fl = flop_estimate(rows, cols, ell, q)
     val = fl / t / 1e9
-    cores = os.cpu_count()
+    cores = host_cores()
     line = {
         "impl": "reference", "metric": "corutv_gflops", "value": round(val, 3), "unit": "GFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -293,10 +310,17 @@ def main():
     from paper_1906_04572_b200 import _lib
     from paper_1906_04572_b200.dist import RowShardComm, corutv_sharded, row_range
 
+    # one rank per GPU; CORUTV_BENCH_BACKEND=gloo (and more ranks than GPUs)
+    # is only for dry runs of the multi-rank logic on a one-GPU box
+    backend = os.environ.get("CORUTV_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        tdist.init_process_group("nccl", device_id=device)
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=device)
+        else:
+            tdist.init_process_group(backend)
     wl = args.workload
     m, n, ell, q, *_ = WORKLOADS[wl]
     lo, hi = row_range(m, world, rank)
@@ -333,19 +357,37 @@ def main():
     h.bind_stream()
     h.lib.corutv_profile_begin(h.ptr)
     stream = torch.cuda.current_stream(device)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        f = step(a, omega)
-    e1.record(stream)
+    # A per rank larger than twice the 126 MB L2: steps run back to back.
+    # Smaller (C1, C2): every step is timed on its own events and L2 is
+    # flushed between steps by writing a 512 MB buffer (outside the events).
+    l2_resident = 8 * (hi - lo) * n < 2 * 126 * 2 ** 20
+    flush = torch.empty(2 ** 26, dtype=torch.float64, device=device) if l2_resident else None
+    step_ms = []
+    if not l2_resident:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            f = step(a, omega)
+        e1.record(stream)
+    else:
+        evs = []
+        for _ in range(args.steps):
+            flush.fill_(0.0)
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            b0.record(stream)
+            f = step(a, omega)
+            b1.record(stream)
+            evs.append((b0, b1))
     torch.cuda.synchronize()
+    if l2_resident:
+        step_ms = [b0.elapsed_time(b1) for b0, b1 in evs]
     barrier()
     torch.cuda.synchronize()
     prof = (ctypes.c_double * 12)()
     nl = ctypes.c_int64(0)
     h.lib.corutv_profile_end(h.ptr, prof, ctypes.byref(nl))
     clk = clocks.stop()
-    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    ms = max_over_ranks(sum(step_ms) / args.steps if l2_resident else e0.elapsed_time(e1) / args.steps)
     flops = flop_estimate(m, n, ell, q)
     value = flops / (ms / 1e3) / 1e9
 
@@ -424,13 +466,14 @@ def main():
         rows, cols = cpu_sample(wl)
         sample = gen_rows_host(wl, rows, cols=cols)
         om = O.gaussian_matrix(cols, ell, 0)
-        t0 = time.perf_counter()
-        O.corutv(sample, ell, q, omega=om)
-        tc = time.perf_counter() - t0
+        with all_blas_threads():
+            t0 = time.perf_counter()
+            O.corutv(sample, ell, q, omega=om)
+            tc = time.perf_counter() - t0
         cpu = {"value": round(flop_estimate(rows, cols, ell, q) / tc / 1e9, 3), "unit": "GFLOP/s",
-               "cores": os.cpu_count(), "kind": "port",
-               "sample": f"oracle (numpy restatement of corutv, OpenBLAS) on a {rows}x{cols} block of "
-                         f"the {wl} distribution, ell={ell}, q={q}, 1 run, {tc:.2f} s"}
+               "cores": host_cores(), "kind": "port",
+               "sample": f"oracle (numpy restatement of corutv, OpenBLAS {host_cores()} threads) on a "
+                         f"{rows}x{cols} block of the {wl} distribution, ell={ell}, q={q}, 1 run, {tc:.2f} s"}
 
     if rank == 0:
         line = {
@@ -441,7 +484,9 @@ def main():
             "config": {"workload": wl, "desc": WORKLOADS[wl][6], "m": m, "n": n, "ell": ell, "q": q,
                        "variant": "exact-d", "rows_per_rank": hi - lo,
                        "parallelism": f"row-shard x{world}" if world > 1 else "single",
-                       "l2": "inputs larger than L2 (A = %.1f GB)" % (8 * m * n / 1e9),
+                       "l2": ("L2 flushed between steps (512 MB write), steps timed individually (A = %.3f GB)"
+                              % (8 * m * n / 1e9)) if l2_resident else
+                             "inputs larger than L2 (A = %.1f GB)" % (8 * m * n / 1e9),
                        "flops_per_step": flops, "omega": "seeded numpy PCG64, resident on device"},
             "fp64_pct_of_peak": round(100 * value / 1e3 / result["roofline"]["peak"], 2),
             "roofline": result["roofline"],
