@@ -601,9 +601,14 @@ void qrcp(corutv_handle* h, const double* D, int l, int64_t ldd, double* T, int6
   const size_t one = (size_t)l * l * 8;
   const size_t stat128 = 5 * 128 * 8 + 4 * 128 * 4 + 1024;
   if (l <= 128 && 2 * one + stat128 <= (size_t)optin) {
-    const int G = l <= 64 ? 4 : 2;
+    static const int g_env = [] {
+      const char* e = std::getenv("CORUTV_QRCP_G");  // tuning knob
+      return e ? std::atoi(e) : 0;
+    }();
+    const int G = g_env ? g_env : (l <= 64 ? 4 : 2);
     const int threads = (int)std::min<int64_t>(1024, round_up((int64_t)l * G, 32));
-    auto kern = (G == 4) ? small::qrcp_kernel<128, 4> : small::qrcp_kernel<128, 2>;
+    auto kern = (G == 8) ? small::qrcp_kernel<128, 8>
+                         : ((G == 4) ? small::qrcp_kernel<128, 4> : small::qrcp_kernel<128, 2>);
     set_smem(h, kern, 2 * one);
     kern<<<1, threads, 2 * one, h->stream>>>(D, l, ldd, T, ldt, qtT, ldq, perm_out, perm32, gwork, 1, 1, delta,
                                              r_dev);
@@ -655,10 +660,15 @@ void jacobi(corutv_handle* h, const double* X, int nv, int len, int64_t ldx, dou
   const int optin = max_optin_smem(h);
   const size_t stat = (small::LMAX * 2) * 8 + 8 * 1024;
   const bool smem = bytes + stat <= (size_t)optin;
-  if (smem) set_smem(h, small::jacobi_kernel, bytes);
   const int jt = (int)std::min<int64_t>(1024, std::max<int64_t>(64, 32 * (int64_t)((n + 1) / 2)));
-  small::jacobi_kernel<<<1, jt, smem ? bytes : 0, h->stream>>>(
-      X, nv, len, ldx, 1e-14, 100, sig, pinv, ldp, ut, ldut, vt, ldvt, gwork, smem ? 1 : 0, status);
+  if (smem) {
+    set_smem(h, small::jacobi_kernel<true>, bytes);
+    small::jacobi_kernel<true><<<1, jt, bytes, h->stream>>>(X, nv, len, ldx, 1e-14, 100, sig, pinv, ldp, ut, ldut,
+                                                             vt, ldvt, gwork, 1, status);
+  } else {
+    small::jacobi_kernel<false><<<1, jt, 0, h->stream>>>(X, nv, len, ldx, 1e-14, 100, sig, pinv, ldp, ut, ldut,
+                                                          vt, ldvt, gwork, 0, status);
+  }
   CK_LAUNCH();
 }
 

@@ -1,6 +1,8 @@
-// Small dense kernels on l x l (l <= ~600) matrices, one CTA each, working in
-// shared memory when the matrix fits and in (L2-resident) global scratch
-// otherwise — the pointer is generic either way.
+// Small dense kernels on l x l matrices, one CTA each.  The Cholesky and QRCP
+// kernels work entirely in shared memory (larger cores go to the cluster
+// versions); the Jacobi kernel is compiled for shared or (L2-resident)
+// global scratch as a template parameter, so every access has a known
+// address space (LDS/STS, never generic LD/ST).
 //
 //   chol_factor_kernel : R = chol(G [+ s I]), R^-1, kappa_F — one step of the
 //                        adaptive shifted CholeskyQR that replaces
@@ -45,167 +47,14 @@ struct CholInfo {
   double trace;
 };
 
-// Blocked Cholesky of the augmented matrix [G | I] (row-major, ld = 2l):
-// the row operations that turn G into R (R'R = G) turn I into R^-T, so the
-// right half ends up holding rinvT[j][k] = R^-1[k][j] -- exactly the Bt
-// operand of the X * R^-1 GEMM -- without a separate triangular inverse.
-// Panels of NB rows: (a) one warp factors the NB x NB diagonal block,
-// (b) thread-per-column forward substitution applies D^-T to the panel's
-// rows (left trailing columns + right-half columns 0..kb+nb-1), (c) the
-// trailing rows get the Schur update in 4 x 4 register tiles (upper
-// triangle on the left, lower-triangular nonzero band on the right).
-// W may be shared or global memory (generic pointer); in global mode the
-// panel rows are staged in shared memory (`stage`).
+// The augmented matrix [G | I] (row-major, ld = 2l): the row operations
+// that turn G into R (R'R = G) turn I into R^-T, so the right half ends up
+// holding rinvT[j][k] = R^-1[k][j] -- exactly the Bt operand of the X * R^-1
+// GEMM -- without a separate triangular inverse.  NB: panel height of the
+// cluster version (chol_cluster.cuh).
 constexpr int NB = 32;
 
-// One warp factors the nb x nb (nb <= 32) upper block whose columns come
-// from `load(i, k)` (row i, column k, i <= k < nb), keeping column `lane` in
-// registers and broadcasting row j with shuffles (fully unrolled: static
-// register indices).  Out-of-range rows/columns are identity-padded.
-// Returns the factor column in c[] (c[i] = R[i][lane], i <= lane) and a
-// warp-uniform failure flag.
-template <typename Load>
-__device__ __forceinline__ bool warp_chol32(double (&c)[32], int nb, Load load) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int i = 0; i < 32; ++i)
-    c[i] = (lane < nb && i < nb) ? ((i <= lane) ? load(i, lane) : 0.0) : (i == lane ? 1.0 : 0.0);
-  bool bad = false;
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const double d = __shfl_sync(0xffffffffu, c[j], j);
-    bad |= !(d > 0.0) || !isfinite(d);
-    const double r = sqrt(d);
-    double cj = c[j];
-    if (lane > j) cj = cj / r;
-    else if (lane == j) cj = r;
-    c[j] = cj;
-#pragma unroll
-    for (int i = j + 1; i < 32; ++i) {
-      const double rji = __shfl_sync(0xffffffffu, cj, i);
-      if (lane >= i) c[i] = fma(-rji, cj, c[i]);
-    }
-  }
-  return bad;
-}
-
-__device__ __forceinline__ void tile_update(double* W, int ld, const double* P, int pld,
-                                            int pcol0, int nb, int i0, int k0, int imax,
-                                            int kmax, bool upper, int roff) {
-  // W[i][k] -= sum_p P[p][i - pcol0] * P[p][k - pcol0 + roff] for the 4x4 tile
-  double acc[4][4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
-  for (int p = 0; p < nb; ++p) {
-    const double* row = P + (int64_t)p * pld;
-    double a[4], b[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) a[r] = (i0 + r < imax) ? row[i0 + r - pcol0] : 0.0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) b[c] = (k0 + c < kmax) ? row[k0 + c - pcol0 + roff] : 0.0;
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[r][c] = fma(a[r], b[c], acc[r][c]);
-  }
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int i = i0 + r;
-    if (i >= imax) continue;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int k = k0 + c;
-      if (k >= kmax || (upper && k < i)) continue;
-      W[(int64_t)i * ld + k + (upper ? 0 : roff)] -= acc[r][c];
-    }
-  }
-}
-
-// Returns true on failure (non-positive / non-finite pivot), uniformly.
-__device__ bool chol_aug_blocked(double* W, int l, bool wglobal, double* stage, int* s_flag) {
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
-  const int ld = 2 * l;
-  for (int kb = 0; kb < l; kb += NB) {
-    const int nb = min(NB, l - kb);
-    // (a) diagonal block, warp 0 (lane = column inside the block)
-    if (warp == 0) {
-      double c[32];
-      const bool bad = warp_chol32(c, nb, [&](int i, int k) { return W[(int64_t)(kb + i) * ld + kb + k]; });
-#pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (i <= lane && lane < nb) W[(int64_t)(kb + i) * ld + kb + lane] = c[i];
-      if (lane == 0) *s_flag = bad ? 1 : 0;
-    }
-    __syncthreads();
-    if (*s_flag) return true;
-    // (b) rows kb..kb+nb  <-  D^-T rows, for left columns [kb+nb, l) and right
-    //     columns [l, l + kb + nb)
-    const int c0 = kb + nb;
-    const int nleft = l - c0, nright = kb + nb;
-    for (int t = tid; t < nleft + nright; t += nt) {
-      const int c = (t < nleft) ? c0 + t : l + (t - nleft);
-      double x[NB];
-#pragma unroll
-      for (int i = 0; i < NB; ++i) x[i] = (i < nb) ? W[(int64_t)(kb + i) * ld + c] : 0.0;
-#pragma unroll
-      for (int i = 0; i < NB; ++i) {
-        if (i < nb) {
-          double sacc = x[i];
-#pragma unroll
-          for (int q = 0; q < i; ++q) sacc -= W[(int64_t)(kb + q) * ld + kb + i] * x[q];
-          x[i] = sacc / W[(int64_t)(kb + i) * ld + kb + i];
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < NB; ++i)
-        if (i < nb) W[(int64_t)(kb + i) * ld + c] = x[i];
-    }
-    __syncthreads();
-    if (c0 >= l) break;
-    // stage the panel rows (columns [c0, l) and [l, l + nright)) for global W
-    const double* P = W + (int64_t)kb * ld;
-    int pld = ld, pcol0 = 0;
-    if (wglobal) {
-      const int w = nleft + nright;
-      for (int p = warp; p < nb; p += nt >> 5)
-        for (int c = lane; c < w; c += 32) stage[p * w + c] = W[(int64_t)(kb + p) * ld + c0 + c];
-      __syncthreads();
-      P = stage;
-      pld = w;
-      pcol0 = c0;
-    }
-    // (c) trailing rows i in [c0, l):
-    //     left  : W[i][k] -= sum_p P[p][i] P[p][k],   i <= k < l
-    //     right : W[i][l + k'] -= sum_p P[p][i] P[p][l + k'],  k' < nright
-    const int TI = (nleft + 3) / 4;
-    const int nup = TI * (TI + 1) / 2;        // upper-triangle 4x4 tiles
-    const int TR = (nright + 3) / 4;
-    const int nrt = TI * TR;                  // right-half tiles
-    // global columns of the staged right part start at pcol0 + nleft
-    const int roff = wglobal ? (nleft - (l - c0)) : 0;  // == 0 by construction
-    for (int t = tid; t < nup + nrt; t += nt) {
-      if (t < nup) {
-        int tk = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-        while ((tk + 1) * (tk + 2) / 2 <= t) ++tk;
-        while (tk * (tk + 1) / 2 > t) --tk;
-        const int ti = t - tk * (tk + 1) / 2;
-        tile_update(W, ld, P, pld, pcol0, nb, c0 + 4 * ti, c0 + 4 * tk, l, l, true, 0);
-      } else {
-        const int u = t - nup;
-        const int ti = u / TR, tk = u % TR;
-        // right-half column k' lives at W column l + k' and staged column
-        // (l - c0) + k' (global mode) or l + k' (shared mode)
-        tile_update(W, ld, P, pld, pcol0, nb, c0 + 4 * ti, l + 4 * tk, l, l + nright, false, roff);
-      }
-    }
-    __syncthreads();
-  }
-  return false;
-}
-
-// Unblocked right-looking Cholesky of [G | I] in shared memory (l <= ~113):
+// Unblocked right-looking Cholesky of [G | I] in shared memory (l < 64):
 // two barriers per column, the trailing update spread over warps (rows) and
 // lanes (columns) with no serial chains -- latency-optimal for small cores.
 __device__ bool chol_aug_unblocked(double* W, int l) {
@@ -258,8 +107,12 @@ __global__ void __launch_bounds__(512, 1)
   extern __shared__ double dsm[];
   __shared__ double red[NWARPS];
   __shared__ int s_flag;
-  double* W = use_smem ? dsm : gwork;
-  double* stage = use_smem ? nullptr : dsm;
+  // [G | I] always in shared memory here (the host launches this kernel only
+  // when it fits; larger cores use the cluster kernel), so every access is
+  // an LDS/STS rather than a generic LD/ST
+  (void)use_smem;
+  (void)gwork;
+  double* W = dsm;
   const int ld = 2 * l;
   double tr = 0.0;
   for (int i = threadIdx.x; i < l; i += blockDim.x) tr += G[i * ldg + i];
@@ -289,7 +142,7 @@ __global__ void __launch_bounds__(512, 1)
           W[(int64_t)i * ld + k] = g;
         }
       __syncthreads();
-      const bool fail = use_smem ? chol_aug_unblocked(W, l) : chol_aug_blocked(W, l, true, stage, &s_flag);
+      const bool fail = chol_aug_unblocked(W, l);
       __syncthreads();
       if (fail) {
         if (!shifted) { shifted = 1; continue; }
@@ -473,8 +326,14 @@ __global__ void __launch_bounds__(1024, 1)
   __shared__ int has_ref[LM];
   const int lane = threadIdx.x & 31;
   const int nt = blockDim.x;
-  double* R = smem_R ? dsm : gwork;
-  double* Q = smem_Q ? (smem_R ? dsm + l * l : dsm) : gwork + (int64_t)l * l;
+  // R and Q always in shared memory here (the host launches this kernel
+  // only when they fit); a pointer chosen at run time between shared and
+  // global memory would compile every access to a generic LD/ST
+  (void)smem_R;
+  (void)smem_Q;
+  (void)gwork;
+  double* R = dsm;
+  double* Q = dsm + l * l;
 
   for (int i = threadIdx.x >> 5; i < l; i += nt >> 5)
     for (int c = lane; c < l; c += 32) R[i * l + c] = D[i * ldd + c];
@@ -516,6 +375,7 @@ __global__ void __launch_bounds__(1024, 1)
 // sig (device, nv, descending).  pinv != nullptr: B = X^T (len x nv) and
 // pinv(B) (nv x len, ld ldp) is written with the cutoff
 // max(len, nv) * sig0 * 1e-12 (dense.py:390-402).
+template <bool USE_SMEM>
 __global__ void __launch_bounds__(THREADS, 1)
     jacobi_kernel(const double* __restrict__ X, int nv, int len, int64_t ldx, double tol,
                   int max_sweeps, double* sig_out, double* pinv, int64_t ldp, double* ut_out,
@@ -530,7 +390,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int nt = blockDim.x;
   const int n = nv + (nv > 1 && (nv & 1));  // pad odd counts with a zero row
   const bool want_v = pinv != nullptr || vt_out != nullptr;
-  double* W = use_smem ? dsm : gwork;          // n x len
+  (void)use_smem;
+  double* W = USE_SMEM ? dsm : gwork;          // n x len (compile-time address space)
   double* V = W + (int64_t)n * len;            // n x n (row a = column a of V)
   for (int r = warp; r < n; r += nwarps)
     for (int c = lane; c < len; c += 32) W[(int64_t)r * len + c] = (r < nv) ? X[r * ldx + c] : 0.0;
