@@ -99,14 +99,13 @@ __device__ double upper_sumsq(const double* W, int l, int ld, int col0, bool low
 // CholeskyQR, Fukaya et al. 2020).  allow_plain: try the unshifted factor
 // first and keep it when it succeeds with kappa_F <= kappa_max.
 // Output rinvT (l x l, ld ldr): rinvT[j][k] = R^-1[k][j] (the Bt operand of
-// the X * R^-1 GEMM).  Work: [G | I], 2 l^2 doubles (shared or global).
+// the X * R^-1 GEMM).  Work: [G | I], 2 l^2 doubles of shared memory.
 __global__ void __launch_bounds__(512, 1)
     chol_factor_kernel(const double* __restrict__ G, int l, int64_t ldg, double shift_coeff,
                        int allow_plain, double kappa_max, double* __restrict__ rinvT,
                        int64_t ldr, double* gwork, int use_smem, CholInfo* info) {
   extern __shared__ double dsm[];
   __shared__ double red[NWARPS];
-  __shared__ int s_flag;
   // [G | I] always in shared memory here (the host launches this kernel only
   // when it fits; larger cores use the cluster kernel), so every access is
   // an LDS/STS rather than a generic LD/ST
