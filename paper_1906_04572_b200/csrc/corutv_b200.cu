@@ -244,13 +244,24 @@ bool make_map3d(corutv_handle* h, const double* base, int64_t cols, int64_t rows
 // ------------------------------------------------------------------- GEMM
 struct GemmPlan {
   int J, n_tiles, m_tiles, k_tiles, splits, kps;
+  int WN = 2;  // warps along N: 2 -> CTA 128 x 16J; 1 -> CTA 256 x 8J (N <= 64)
 };
 
 GemmPlan plan_gemm(const corutv_handle* h, int64_t M, int64_t N, int64_t K, bool allow_split) {
   GemmPlan p;
-  p.n_tiles = (int)((N + 127) / 128);
-  p.J = (int)std::min<int64_t>(8, std::max<int64_t>(1, (N + 16 * p.n_tiles - 1) / (16 * p.n_tiles)));
-  p.m_tiles = (int)((M + gemm::BM - 1) / gemm::BM);
+  if (N <= 64) {
+    // narrow products (spectral-norm blocks, small ALM samples): 8-column
+    // granularity, e.g. N = 24 computes 24 columns instead of 32
+    p.WN = 1;
+    p.n_tiles = 1;
+    p.J = (int)std::max<int64_t>(1, (N + 7) / 8);
+  } else {
+    p.WN = 2;
+    p.n_tiles = (int)((N + 127) / 128);
+    p.J = (int)std::min<int64_t>(8, std::max<int64_t>(1, (N + 16 * p.n_tiles - 1) / (16 * p.n_tiles)));
+  }
+  const int bm = gemm::bm_of(p.WN);
+  p.m_tiles = (int)((M + bm - 1) / bm);
   p.k_tiles = (int)((K + gemm::BK - 1) / gemm::BK);
   const int64_t base = (int64_t)p.m_tiles * p.n_tiles;
   const int sms = h->num_sms;
@@ -274,33 +285,40 @@ GemmPlan plan_gemm(const corutv_handle* h, int64_t M, int64_t N, int64_t K, bool
   return p;
 }
 
-template <int J, bool MM, bool CHECK>
+template <int J, bool MM, bool CHECK, int WN>
 void launch_gemm_t(corutv_handle* h, const CUtensorMap& ma, const CUtensorMap& mb, const gemm::Tile& t,
                    const gemm::StoreParams& sp, int grid) {
-  auto kern = gemm::gemm_kernel<J, MM, CHECK>;
+  auto kern = gemm::gemm_kernel<J, MM, CHECK, WN>;
   static bool configured = false;
   if (!configured) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::smem_bytes(J)));
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::smem_bytes(J, WN)));
     configured = true;
   }
   ProfScope ps(h, h->tag, 2.0 * t.M * t.N * (double)t.K);
-  kern<<<grid, gemm::THREADS, gemm::smem_bytes(J), h->stream>>>(ma, mb, t, sp);
+  kern<<<grid, gemm::THREADS, gemm::smem_bytes(J, WN), h->stream>>>(ma, mb, t, sp);
   CK_LAUNCH();
 }
 
-template <bool MM, bool CHECK>
-void launch_gemm_j(corutv_handle* h, int J, const CUtensorMap& ma, const CUtensorMap& mb,
+template <bool MM, bool CHECK, int WN>
+void launch_gemm_w(corutv_handle* h, int J, const CUtensorMap& ma, const CUtensorMap& mb,
                    const gemm::Tile& t, const gemm::StoreParams& sp, int grid) {
   switch (J) {
-    case 1: launch_gemm_t<1, MM, CHECK>(h, ma, mb, t, sp, grid); break;
-    case 2: launch_gemm_t<2, MM, CHECK>(h, ma, mb, t, sp, grid); break;
-    case 3: launch_gemm_t<3, MM, CHECK>(h, ma, mb, t, sp, grid); break;
-    case 4: launch_gemm_t<4, MM, CHECK>(h, ma, mb, t, sp, grid); break;
-    case 5: launch_gemm_t<5, MM, CHECK>(h, ma, mb, t, sp, grid); break;
-    case 6: launch_gemm_t<6, MM, CHECK>(h, ma, mb, t, sp, grid); break;
-    case 7: launch_gemm_t<7, MM, CHECK>(h, ma, mb, t, sp, grid); break;
-    default: launch_gemm_t<8, MM, CHECK>(h, ma, mb, t, sp, grid); break;
+    case 1: launch_gemm_t<1, MM, CHECK, WN>(h, ma, mb, t, sp, grid); break;
+    case 2: launch_gemm_t<2, MM, CHECK, WN>(h, ma, mb, t, sp, grid); break;
+    case 3: launch_gemm_t<3, MM, CHECK, WN>(h, ma, mb, t, sp, grid); break;
+    case 4: launch_gemm_t<4, MM, CHECK, WN>(h, ma, mb, t, sp, grid); break;
+    case 5: launch_gemm_t<5, MM, CHECK, WN>(h, ma, mb, t, sp, grid); break;
+    case 6: launch_gemm_t<6, MM, CHECK, WN>(h, ma, mb, t, sp, grid); break;
+    case 7: launch_gemm_t<7, MM, CHECK, WN>(h, ma, mb, t, sp, grid); break;
+    default: launch_gemm_t<8, MM, CHECK, WN>(h, ma, mb, t, sp, grid); break;
   }
+}
+
+template <bool MM, bool CHECK>
+void launch_gemm_j(corutv_handle* h, int J, int WN, const CUtensorMap& ma, const CUtensorMap& mb,
+                   const gemm::Tile& t, const gemm::StoreParams& sp, int grid) {
+  if (WN == 1) launch_gemm_w<MM, CHECK, 1>(h, J, ma, mb, t, sp, grid);
+  else launch_gemm_w<MM, CHECK, 2>(h, J, ma, mb, t, sp, grid);
 }
 
 void launch_grid_1d(int64_t total, int* blocks, int* threads) {
@@ -342,6 +360,7 @@ void run_gemm(corutv_handle* h, bool mm, int64_t M, int64_t N, int64_t K, const 
     p.splits = force->splits;
     p.kps = force->kps;
   }
+  const int bm = gemm::bm_of(p.WN), bn = gemm::bn_of(p.J, p.WN);
   gemm::Tile t;
   t.M = (int)M;
   t.N = (int)N;
@@ -354,9 +373,10 @@ void run_gemm(corutv_handle* h, bool mm, int64_t M, int64_t N, int64_t K, const 
   CUtensorMap ma, mb;
   t.mm3d = 0;
   if (!mm) {
-    ma = make_map(h, A, K, M, lda, gemm::BM);
-    mb = make_map(h, B, K, N, ldb, 16 * p.J);
-  } else if (make_map3d(h, A, M, K, lda, gemm::BM / 16, &ma) && make_map3d(h, B, N, K, ldb, p.J, &mb)) {
+    ma = make_map(h, A, K, M, lda, bm);
+    mb = make_map(h, B, K, N, ldb, bn);
+  } else if (make_map3d(h, A, M, K, lda, bm / 16, &ma) &&
+             make_map3d(h, B, N, K, ldb, gemm::nb16_of(p.J, p.WN), &mb)) {
     t.mm3d = 1;
   } else {
     ma = make_map(h, A, M, K, lda, gemm::BK);
@@ -364,8 +384,8 @@ void run_gemm(corutv_handle* h, bool mm, int64_t M, int64_t N, int64_t K, const 
   }
   static const bool debug_plan = std::getenv("CORUTV_DEBUG_PLAN") != nullptr;
   if (debug_plan)
-    std::fprintf(stderr, "[corutv] gemm %s M=%lld N=%lld K=%lld J=%d tiles=%dx%d splits=%d kps=%d mm3d=%d\n",
-                 mm ? "MM" : "KK", (long long)M, (long long)N, (long long)K, p.J, p.m_tiles, p.n_tiles, p.splits,
+    std::fprintf(stderr, "[corutv] gemm %s M=%lld N=%lld K=%lld J=%d WN=%d tiles=%dx%d splits=%d kps=%d mm3d=%d\n",
+                 mm ? "MM" : "KK", (long long)M, (long long)N, (long long)K, p.J, p.WN, p.m_tiles, p.n_tiles, p.splits,
                  p.kps, t.mm3d);
   const bool direct = (p.splits == 1 && Ct == nullptr && C != nullptr);
   const int64_t ldw = round_up(N, 2);
@@ -382,11 +402,11 @@ void run_gemm(corutv_handle* h, bool mm, int64_t M, int64_t N, int64_t K, const 
   }
   const int grid = p.m_tiles * p.n_tiles * p.splits;
   if (mm) {
-    if (bad_flag) launch_gemm_j<true, true>(h, p.J, ma, mb, t, sp, grid);
-    else launch_gemm_j<true, false>(h, p.J, ma, mb, t, sp, grid);
+    if (bad_flag) launch_gemm_j<true, true>(h, p.J, p.WN, ma, mb, t, sp, grid);
+    else launch_gemm_j<true, false>(h, p.J, p.WN, ma, mb, t, sp, grid);
   } else {
-    if (bad_flag) launch_gemm_j<false, true>(h, p.J, ma, mb, t, sp, grid);
-    else launch_gemm_j<false, false>(h, p.J, ma, mb, t, sp, grid);
+    if (bad_flag) launch_gemm_j<false, true>(h, p.J, p.WN, ma, mb, t, sp, grid);
+    else launch_gemm_j<false, false>(h, p.J, p.WN, ma, mb, t, sp, grid);
   }
   if (!direct) {
     launch_grid_1d(M * N, &nb, &tb);

@@ -27,14 +27,24 @@ constexpr int NCW = 8;                 // warps (all compute; thread 0 also issu
 constexpr int THREADS = NCW * 32;       // 2 warps per SMSP -> up to 255 registers each
 constexpr int SMEM_BUDGET = 200 * 1024;
 
-__host__ __device__ constexpr int a_stage_bytes() { return BM * BK * 8; }
-__host__ __device__ constexpr int b_stage_bytes(int J) { return 16 * J * BK * 8; }
-__host__ __device__ constexpr int stage_bytes(int J) { return a_stage_bytes() + b_stage_bytes(J); }
-__host__ __device__ constexpr int num_stages(int J) {
-  return (SMEM_BUDGET - 1024) / stage_bytes(J) > 8 ? 8 : (SMEM_BUDGET - 1024) / stage_bytes(J);
+// WN = warps along N: 2 (CTA 128 x 16J, the default) or 1 (CTA 256 x 8J, for
+// narrow N <= 64: an 8-column granularity instead of 16 halves the padding)
+__host__ __device__ constexpr int bm_of(int WN) { return 32 * (NCW / WN); }       // CTA rows
+__host__ __device__ constexpr int bn_of(int J, int WN) { return 8 * J * WN; }     // CTA columns
+__host__ __device__ constexpr int nb16_of(int J, int WN) { return (bn_of(J, WN) + 15) / 16; }
+__host__ __device__ constexpr int a_stage_bytes(int WN = 2) { return bm_of(WN) * BK * 8; }
+// B slot: room for the 16-column boxes of the MM layout (>= the KK rows)
+__host__ __device__ constexpr int b_stage_bytes(int J, int WN = 2) { return nb16_of(J, WN) * 16 * BK * 8; }
+__host__ __device__ constexpr int stage_bytes(int J, int WN = 2) { return a_stage_bytes(WN) + b_stage_bytes(J, WN); }
+// bytes TMA actually writes per stage (the mbarrier transaction count)
+__host__ __device__ constexpr int stage_tx(int J, int WN, bool MM) {
+  return a_stage_bytes(WN) + (MM ? b_stage_bytes(J, WN) : bn_of(J, WN) * BK * 8);
 }
-__host__ __device__ constexpr int smem_bytes(int J) {
-  return 1024 /*align slack*/ + num_stages(J) * stage_bytes(J) + 2 * 8 * 8 + 64;
+__host__ __device__ constexpr int num_stages(int J, int WN = 2) {
+  return (SMEM_BUDGET - 1024) / stage_bytes(J, WN) > 8 ? 8 : (SMEM_BUDGET - 1024) / stage_bytes(J, WN);
+}
+__host__ __device__ constexpr int smem_bytes(int J, int WN = 2) {
+  return 1024 /*align slack*/ + num_stages(J, WN) * stage_bytes(J, WN) + 2 * 8 * 8 + 64;
 }
 // low-rank (ALM / residual / store) kernels: K = r is short, so 2 stages; the
 // same bytes are reused to stage the 128 x (16J + 2) result tile.
@@ -75,26 +85,27 @@ struct Smem {
 
 // Pointer arithmetic on the __shared__ array (never through an integer) so
 // the compiler keeps the shared address space and emits LDS.
-template <int J, int S, int DATA = S * (a_stage_bytes() + b_stage_bytes(J))>
+template <int J, int S, int DATA = S * (a_stage_bytes() + b_stage_bytes(J)), int WN = 2>
 __device__ __forceinline__ Smem carve(unsigned char* raw) {
   const uint32_t pad = (1024u - (smem_u32(raw) & 1023u)) & 1023u;
   unsigned char* p = raw + pad;
   Smem s;
   s.a = reinterpret_cast<double*>(p);
-  s.b = reinterpret_cast<double*>(p + S * a_stage_bytes());
+  s.b = reinterpret_cast<double*>(p + S * a_stage_bytes(WN));
   s.full = reinterpret_cast<uint64_t*>(p + DATA);
   s.empty = s.full + 8;
   return s;
 }
 
 // Issue the TMA loads of k tile `kt` into ring slot `st` (thread 0 only).
-template <int J, bool MM>
+template <int J, bool MM, int WN = 2>
 __device__ __forceinline__ void issue_stage(const Smem& sm, const CUtensorMap* mapA,
                                             const CUtensorMap* mapB, int m0, int n0, int kt,
                                             int st, int mm3d = 0) {
-  mbar_arrive_expect_tx(&sm.full[st], stage_bytes(J));
-  double* sa = sm.a + st * (BM * BK);
-  double* sb = sm.b + st * (16 * J * BK);
+  constexpr int BMW = bm_of(WN), NB16 = nb16_of(J, WN);
+  mbar_arrive_expect_tx(&sm.full[st], stage_tx(J, WN, MM));
+  double* sa = sm.a + st * (BMW * BK);
+  double* sb = sm.b + st * (NB16 * 16 * BK);
   if (!MM) {
     tma_load_2d(sa, mapA, &sm.full[st], kt * BK, m0);
     tma_load_2d(sb, mapB, &sm.full[st], kt * BK, n0);
@@ -104,10 +115,10 @@ __device__ __forceinline__ void issue_stage(const Smem& sm, const CUtensorMap* m
     tma_load_3d(sb, mapB, &sm.full[st], 0, kt * BK, n0 / 16);
   } else {
 #pragma unroll
-    for (int bx = 0; bx < BM / 16; ++bx)
+    for (int bx = 0; bx < BMW / 16; ++bx)
       tma_load_2d(sa + bx * 16 * BK, mapA, &sm.full[st], m0 + 16 * bx, kt * BK);
 #pragma unroll
-    for (int bx = 0; bx < J; ++bx)
+    for (int bx = 0; bx < NB16; ++bx)
       tma_load_2d(sb + bx * 16 * BK, mapB, &sm.full[st], n0 + 16 * bx, kt * BK);
   }
 }
@@ -127,7 +138,7 @@ __device__ __forceinline__ void issue_stage(const Smem& sm, const CUtensorMap* m
 // MM: both operands M-major (16-column boxes, rows = k); lanes read rows
 //     k = s + 4(lane&3): the 4 rows of a fragment fall on two different
 //     (k & 7) swizzle phases, 2 wavefronts per 256 B, the minimum.
-template <int J, bool MM, bool CHECK, int S = num_stages(J)>
+template <int J, bool MM, bool CHECK, int S = num_stages(J), int WN = 2>
 __device__ __forceinline__ void mainloop(const Smem& sm, const CUtensorMap* mapA,
                                          const CUtensorMap* mapB, int m0, int n0, int kt0,
                                          int kt1, Acc<J>& acc, int wm, int wn, int lane, int nvf,
@@ -139,7 +150,7 @@ __device__ __forceinline__ void mainloop(const Smem& sm, const CUtensorMap* mapA
   if (leader) {
     tma_prefetch_desc(mapA);
     tma_prefetch_desc(mapB);
-    for (int i = 0; i < S && i < nkt; ++i) issue_stage<J, MM>(sm, mapA, mapB, m0, n0, kt0 + i, i, mm3d);
+    for (int i = 0; i < S && i < nkt; ++i) issue_stage<J, MM, WN>(sm, mapA, mapB, m0, n0, kt0 + i, i, mm3d);
   }
   const int r8 = lane >> 2, c4 = lane & 3;
   // per-lane element offsets (in doubles) inside one stage
@@ -164,11 +175,11 @@ __device__ __forceinline__ void mainloop(const Smem& sm, const CUtensorMap* mapA
     if (leader && i >= 1 && (i - 1) + S < nkt) {
       const int ps = (i - 1) % S;
       mbar_wait(&sm.empty[ps], ((i - 1) / S) & 1);
-      issue_stage<J, MM>(sm, mapA, mapB, m0, n0, kt0 + (i - 1) + S, ps, mm3d);
+      issue_stage<J, MM, WN>(sm, mapA, mapB, m0, n0, kt0 + (i - 1) + S, ps, mm3d);
     }
     mbar_wait(&sm.full[st], ph);
-    const double* sa = sm.a + st * (BM * BK);
-    const double* sb = sm.b + st * (16 * J * BK);
+    const double* sa = sm.a + st * (bm_of(WN) * BK);
+    const double* sb = sm.b + st * (nb16_of(J, WN) * 16 * BK);
     if (!MM) {
 #pragma unroll
       for (int p = 0; p < 2; ++p) {
@@ -257,30 +268,32 @@ struct StoreParams {
   int* bad_flag;         // nullable: set to 1 if a non-finite A entry was read
 };
 
-template <int J, bool MM, bool CHECK>
+template <int J, bool MM, bool CHECK, int WN = 2>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                 Tile t, StoreParams sp) {
   extern __shared__ unsigned char smem_raw[];
-  Smem sm = carve<J, num_stages(J)>(smem_raw);
+  constexpr int S = num_stages(J, WN);
+  Smem sm = carve<J, S, S * stage_bytes(J, WN), WN>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bid = blockIdx.x;
   const int nt = bid % t.n_tiles;
   const int rest = bid / t.n_tiles;
-  const int m0 = (rest % t.m_tiles) * BM;
+  const int m0 = (rest % t.m_tiles) * bm_of(WN);
   const int split = rest / t.m_tiles;
-  const int n0 = nt * 16 * J;
+  const int n0 = nt * bn_of(J, WN);
   const int kt0 = split * t.k_tiles_per_split;
   const int kt1 = min(t.k_tiles, kt0 + t.k_tiles_per_split);
-  init_barriers<num_stages(J)>(sm);
-  const int wm = warp & 3, wn = warp >> 2;
+  init_barriers<S>(sm);
+  constexpr int WMW = NCW / WN;  // warps along M
+  const int wm = warp % WMW, wn = warp / WMW;
   const int ncol0 = n0 + wn * 8 * J;
   const int nvf = max(0, min(J, (t.N - ncol0 + 7) / 8));
   const int mvf = max(0, min(4, (t.M - (m0 + wm * 32) + 7) / 8));
   Acc<J> acc;
   acc.zero();
   bool bad = false;
-  mainloop<J, MM, CHECK>(sm, &mapA, &mapB, m0, n0, kt0, kt1, acc, wm, wn, lane, nvf, mvf, bad, t.mm3d);
+  mainloop<J, MM, CHECK, S, WN>(sm, &mapA, &mapB, m0, n0, kt0, kt1, acc, wm, wn, lane, nvf, mvf, bad, t.mm3d);
   if (CHECK && sp.bad_flag) {
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(sp.bad_flag, 1);
   }
