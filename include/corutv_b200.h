@@ -152,7 +152,8 @@ int corutv_decompose_stream(corutv_handle* h, corutv_read_rows_fn read_rows, voi
 
 /* np.random.Generator(PCG64(seed)).standard_normal((rows, cols)) into out
  * (row-major, ld) on the device, bit-identical (gaussian_matrix,
- * sketch.py:63-68).  Synchronises the stream. */
+ * sketch.py:63-68).  One stream synchronisation (tail-sample readback);
+ * the result is ordered on the handle's stream. */
 int corutv_gaussian(corutv_handle* h, const uint64_t* pcg_state, int64_t rows, int64_t cols,
                     double* out, int64_t ld);
 

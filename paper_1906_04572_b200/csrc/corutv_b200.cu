@@ -51,6 +51,10 @@ struct corutv_handle {
   std::vector<cudaEvent_t> chunk_ev;
   double* staging = nullptr;  // 2 pinned row-chunk buffers (corutv_decompose_stream)
   size_t staging_bytes = 0;   // per buffer
+  // pinned tail-sample scratch of the Gaussian generator: kTailFast entries
+  // of (index, u1, sign) come back with the counts in one readback
+  unsigned char* tails = nullptr;
+  int tails_cap = 0;
   // profiling (corutv_profile_begin/end): launch counter always on; CUDA
   // events around the DMMA GEMM / low-rank kernels while enabled.
   int64_t launches = 0;
@@ -746,11 +750,35 @@ void gaussian(corutv_handle* h, const uint64_t* pcg, int64_t rows, int64_t cols,
   rng::scatter_kernel<<<nb, tb, 0, h->stream>>>(val, starts, tail, rank, P, N, cols, out, ld, outT, ldT, tail_idx,
                                                 tail_u, tail_sign, n_tail, tail_cap);
   CK_LAUNCH();
-  // completeness check (samples available) + tail count, one sync
+  // completeness check (samples available) + tail count, and the first
+  // kTailFast tail records speculatively: one readback in the common case
+  constexpr int kTailFast = 4096;
+  auto ensure_tails = [&](int cap) {
+    if (h->tails_cap >= cap) return;
+    if (h->tails) {
+      sync(h);  // a previous patch copy may still read the old buffer
+      CK(cudaFreeHost(h->tails));
+    }
+    h->tails = nullptr;
+    h->tails_cap = 0;
+    if (cudaMallocHost(&h->tails, (size_t)cap * 20) != cudaSuccess) {
+      cudaGetLastError();
+      fail(h, CORUTV_ERR_NOMEM, "pinned tail scratch allocation failed");
+    }
+    h->tails_cap = cap;
+  };
+  ensure_tails(std::max(kTailFast, h->tails_cap));
+  auto t_idx = [&]() { return reinterpret_cast<int64_t*>(h->tails); };
+  auto t_u = [&]() { return reinterpret_cast<double*>(h->tails + (size_t)h->tails_cap * 8); };
+  auto t_sg = [&]() { return reinterpret_cast<int*>(h->tails + (size_t)h->tails_cap * 16); };
+  const int fast = std::min(kTailFast, tail_cap);
   CK(cudaMemcpyAsync(h->pinned, rank + (P - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaMemcpyAsync(h->pinned + 1, n_tail, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaMemcpyAsync(h->pinned + 2, starts + (P - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaMemcpyAsync(h->pinned + 3, too_long, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(t_idx(), tail_idx, (size_t)fast * 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(t_u(), tail_u, (size_t)fast * 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(t_sg(), tail_sign, (size_t)fast * 4, cudaMemcpyDeviceToHost, h->stream));
   sync(h);
   int64_t total = 0, last = 0;
   unsigned long long ntail = 0;
@@ -764,25 +792,28 @@ void gaussian(corutv_handle* h, const uint64_t* pcg, int64_t rows, int64_t cols,
   if (ntail > (unsigned long long)tail_cap) fail(h, CORUTV_ERR_CUDA, "gaussian: tail overflow");
   if (ntail) {
     const int nt = (int)ntail;
-    std::vector<int64_t> idx(nt);
-    std::vector<double> u(nt);
-    std::vector<int> sg(nt);
-    CK(cudaMemcpyAsync(idx.data(), tail_idx, nt * 8, cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaMemcpyAsync(u.data(), tail_u, nt * 8, cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaMemcpyAsync(sg.data(), tail_sign, nt * 4, cudaMemcpyDeviceToHost, h->stream));
-    sync(h);
+    if (nt > fast) {  // rare: more tails than the speculative readback held
+      ensure_tails(nt);
+      CK(cudaMemcpyAsync(t_idx(), tail_idx, (size_t)nt * 8, cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaMemcpyAsync(t_u(), tail_u, (size_t)nt * 8, cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaMemcpyAsync(t_sg(), tail_sign, (size_t)nt * 4, cudaMemcpyDeviceToHost, h->stream));
+      sync(h);
+    }
     // numpy distributions.c tail: xx = -r^-1 * log1p(-u1); x = +-(r + xx),
     // with the C library's log1p (the same one numpy calls)
+    double* u = t_u();
+    const int* sg = t_sg();
     volatile double neg_inv_r = -zig::kInvR;
     for (int t = 0; t < nt; ++t) {
       const double xx = neg_inv_r * ::log1p(-u[t]);
       const double x = zig::kR + xx;
       u[t] = sg[t] ? -x : x;
     }
-    CK(cudaMemcpyAsync(tail_u, u.data(), nt * 8, cudaMemcpyHostToDevice, h->stream));
+    // the pinned scratch is rewritten only after the next call's readback
+    // sync, which orders it after this copy: no sync needed here
+    CK(cudaMemcpyAsync(tail_u, u, (size_t)nt * 8, cudaMemcpyHostToDevice, h->stream));
     rng::patch_kernel<<<(nt + 255) / 256, 256, 0, h->stream>>>(tail_idx, tail_u, nt, cols, out, ld, outT, ldT);
     CK_LAUNCH();
-    sync(h);  // host vectors go out of scope
   }
 }
 
@@ -1074,7 +1105,7 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
     aux::gather_cols_kernel<<<nb, tb, 0, h->stream>>>(Q2, n, l, ldp, perm32, v, l);
     CK_LAUNCH();
   }
-  sync(h);
+  // no final sync: the outputs are ordered on the stream for the caller
   if (passes_host) *passes_host += passes;
 }
 
@@ -1452,6 +1483,7 @@ void corutv_destroy(corutv_handle* h) {
   if (h->pinned) cudaFreeHost(h->pinned);
   for (cudaEvent_t e : h->chunk_ev) cudaEventDestroy(e);
   if (h->staging) cudaFreeHost(h->staging);
+  if (h->tails) cudaFreeHost(h->tails);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   delete h;
 }
