@@ -138,11 +138,11 @@ def gen_rows_host(wl, rows, seed=99, cols=None):
 
 
 def cpu_sample(wl):
-    """(rows, cols) of the bounded CPU sample: the full matrix for C1/C2, a
-    16384 x 16384 sub-block for C3/C5 (1/16 resp. 1/32 of A, ~3-8 s of
-    16-core OpenBLAS work)."""
+    """(rows, cols) of the bounded CPU sample: the full matrix for C1/C2; for
+    C3/C5 the first 32768 rows at the full 32768 columns (1/4 resp. 1/8 of A,
+    ~10-25 s of 16-core OpenBLAS work)."""
     m, n = WORKLOADS[wl][:2]
-    return {"c1": (m, n), "c2": (m, n), "c3": (16384, 16384), "c5": (16384, 16384)}[wl]
+    return {"c1": (m, n), "c2": (m, n), "c3": (32768, n), "c5": (32768, n)}[wl]
 
 
 # ---------------------------------------------------------------- clocks
