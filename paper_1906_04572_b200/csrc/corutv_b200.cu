@@ -246,6 +246,28 @@ bool make_map3d(corutv_handle* h, const double* base, int64_t cols, int64_t rows
 }
 
 // ------------------------------------------------------------------- GEMM
+// Dynamic shared memory opt-in per kernel function.  Handles on several host
+// threads launch concurrently, so the attribute only ever grows (to the
+// largest request seen), under a lock: a thread lowering it between another
+// thread's set and launch would make that launch invalid.
+std::mutex g_smem_mu;
+std::vector<std::pair<const void*, int>> g_smem_set;
+
+template <typename K>
+void set_smem(corutv_handle* h, K kern, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_smem_mu);
+  const void* key = reinterpret_cast<const void*>(kern);
+  for (auto& e : g_smem_set)
+    if (e.first == key) {
+      if ((size_t)e.second >= bytes) return;
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+      e.second = (int)bytes;
+      return;
+    }
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  g_smem_set.emplace_back(key, (int)bytes);
+}
+
 struct GemmPlan {
   int J, n_tiles, m_tiles, k_tiles, splits, kps;
   int WN = 2;  // warps along N: 2 -> CTA 128 x 16J; 1 -> CTA 256 x 8J (N <= 64)
@@ -293,11 +315,7 @@ template <int J, bool MM, bool CHECK, int WN>
 void launch_gemm_t(corutv_handle* h, const CUtensorMap& ma, const CUtensorMap& mb, const gemm::Tile& t,
                    const gemm::StoreParams& sp, int grid) {
   auto kern = gemm::gemm_kernel<J, MM, CHECK, WN>;
-  static bool configured = false;
-  if (!configured) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::smem_bytes(J, WN)));
-    configured = true;
-  }
+  set_smem(h, kern, gemm::smem_bytes(J, WN));
   ProfScope ps(h, h->tag, 2.0 * t.M * t.N * (double)t.K);
   kern<<<grid, gemm::THREADS, gemm::smem_bytes(J, WN), h->stream>>>(ma, mb, t, sp);
   CK_LAUNCH();
@@ -489,10 +507,7 @@ int max_optin_smem(corutv_handle* h) {
   return v;
 }
 
-template <typename K>
-void set_smem(corutv_handle* h, K kern, size_t bytes) {
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-}
+
 
 // ------------------------------------------------ adaptive CholeskyQR
 // In place of householder_qr(...).q (dense.py:132-149).  Each step: Gram
@@ -538,8 +553,7 @@ void cholqr_multi(corutv_handle* h, QrJob* jobs, int njobs, int ell, int64_t ldx
   if (smem) {
     set_smem(h, small::chol_factor_kernel, aug);
   } else {
-    CK(cudaFuncSetAttribute(chc::chol_factor_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)cl_smem));
+    set_smem(h, chc::chol_factor_cluster_kernel, cl_smem);
     if (cl_cs > 8)
       CK(cudaFuncSetAttribute(chc::chol_factor_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   }
@@ -655,7 +669,7 @@ void qrcp(corutv_handle* h, const double* D, int l, int64_t ldd, double* T, int6
   const size_t dyn = (size_t)cw * l * 8 * (q_smem ? 2 : 1);
   if (cw > qc::MAXCW || dyn + stat > (size_t)optin)
     fail(h, CORUTV_ERR_ARG, "QRCP core too large for a 16-CTA cluster");
-  CK(cudaFuncSetAttribute(qc::qrcp_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+  set_smem(h, qc::qrcp_cluster_kernel, dyn);
   if (cs > 8) CK(cudaFuncSetAttribute(qc::qrcp_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cs, 1, 1);
@@ -1213,11 +1227,7 @@ template <int J, int MODE>
 void launch_lr_t(corutv_handle* h, const CUtensorMap& mu, const CUtensorMap& mw, const gemm::Tile& t,
                  const gemm::LrParams& p, int grid) {
   auto kern = gemm::lowrank_kernel<J, MODE>;
-  static bool configured = false;
-  if (!configured) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::lr_smem_bytes(J)));
-    configured = true;
-  }
+  set_smem(h, kern, gemm::lr_smem_bytes(J));
   ProfScope ps(h, 3, 2.0 * t.M * t.N * (double)t.K);
   kern<<<grid, gemm::THREADS, gemm::lr_smem_bytes(J), h->stream>>>(mu, mw, t, p);
   CK_LAUNCH();

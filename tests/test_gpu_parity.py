@@ -570,3 +570,24 @@ def test_corutv_file_errors(tmp_path):
     matio.write_matrix_bin(p, rng.standard_normal((50, 80)))
     with pytest.raises(ValueError, match="rows >= cols"):
         matio.corutv_file(p, P.SketchConfig(ell=5))
+
+
+def test_concurrent_calls_from_threads_are_bitwise_sequential():
+    """SURVEY 8b threading: the reference harness calls corutv from a
+    ThreadPoolExecutor (bench.py:75-78).  One native handle per thread, the
+    GIL released in the library; results equal the sequential ones."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    rng = np.random.Generator(np.random.PCG64(31))
+    mats = [rng.standard_normal((400 + 50 * i, 20)) @ rng.standard_normal((20, 300)) for i in range(6)]
+    cfgs = [P.SketchConfig(ell=12 + i, q_power=i % 3, seed=i) for i in range(6)]
+    seq = [P.corutv(a, c) for a, c in zip(mats, cfgs)]
+
+    def run(i):
+        torch.cuda.set_device(0)
+        return P.corutv(mats[i], cfgs[i])
+
+    with ThreadPoolExecutor(max_workers=4) as ex:
+        par = list(ex.map(run, range(6)))
+    for f, g in zip(seq, par):
+        assert np.array_equal(f.u, g.u) and np.array_equal(f.t, g.t) and np.array_equal(f.v, g.v)
