@@ -1480,6 +1480,16 @@ int corutv_create(int device, void* stream, corutv_handle** out) {
     return CORUTV_ERR_NOMEM;
   }
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
+  // nested workspaces (e.g. the Gaussian generator inside a decomposition)
+  // come from the device's default stream-ordered pool; keep its memory
+  // mapped across synchronisations, or every call re-maps it (measured:
+  // 40-240 ms stalls in cudaMallocAsync on back-to-back C3 calls)
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
   *out = h;
   return CORUTV_OK;
 }
