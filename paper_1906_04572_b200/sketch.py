@@ -283,11 +283,14 @@ def sor_svd(a, cfg: SketchConfig, counter: PassCounter | None = None, omega=None
     compressed core (corutv_sor_svd)."""
     torch = dev.torch_mod()
     A, was_host = dev.to_device(a, "a")
-    dev.raise_if_nonfinite(A, "a")
     m, n = A.shape
-    if m < n:
-        raise ValueError(f"sor_svd requires rows >= cols, got {m}x{n}")
-    cfg.validated_for(m, n)
+    if m < n or cfg.ell > min(m, n):
+        # reference order: as_matrix's finiteness check comes first (dense.py:48);
+        # otherwise the first sweep flags non-finite entries on the device
+        dev.raise_if_nonfinite(A, "a")
+        if m < n:
+            raise ValueError(f"sor_svd requires rows >= cols, got {m}x{n}")
+        cfg.validated_for(m, n)
     ell = cfg.ell
     u = torch.empty((m, ell), dtype=torch.float64, device=A.device)
     s = torch.empty((ell,), dtype=torch.float64, device=A.device)
@@ -310,9 +313,10 @@ def tsr_svd(a, cfg: SketchConfig, counter: PassCounter | None = None, psi=None, 
     fused sweep)."""
     torch = dev.torch_mod()
     A, was_host = dev.to_device(a, "a")
-    dev.raise_if_nonfinite(A, "a")
     m, n = A.shape
-    cfg.validated_for(m, n)
+    if cfg.ell > min(m, n):
+        dev.raise_if_nonfinite(A, "a")  # reference order (dense.py:48)
+        cfg.validated_for(m, n)
     ell = cfg.ell
     u = torch.empty((m, ell), dtype=torch.float64, device=A.device)
     s = torch.empty((ell,), dtype=torch.float64, device=A.device)
