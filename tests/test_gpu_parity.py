@@ -591,3 +591,32 @@ def test_concurrent_calls_from_threads_are_bitwise_sequential():
         par = list(ex.map(run, range(6)))
     for f, g in zip(seq, par):
         assert np.array_equal(f.u, g.u) and np.array_equal(f.t, g.t) and np.array_equal(f.v, g.v)
+
+
+@pytest.mark.parametrize("shape,ell", [((1, 1), 1), ((5000, 1), 1), ((64, 64), 64), ((300, 7), 7), ((2000, 3), 2)])
+def test_degenerate_shapes_match_oracle(shape, ell):
+    """Single column, 1x1, square with ell = m = n, ell = n (every code path
+    at its boundary): |diag T|, the reconstruction and the pass count."""
+    rng = np.random.Generator(np.random.PCG64(shape[0] + ell))
+    a = rng.standard_normal(shape)
+    for q in (0, 1):
+        cfg = P.SketchConfig(ell=ell, q_power=q, seed=1)
+        cnt = P.PassCounter()
+        f = P.corutv(a, cfg, cnt)
+        ref = O.corutv(a, ell, q, seed=1)
+        assert cnt.passes == ref["passes"]
+        dref = np.abs(np.diag(ref["t"]))
+        assert np.abs(np.abs(np.diag(f.t)) - dref).max() <= 1e-10 * dref[0]
+        err = np.linalg.norm(a - f.lowrank())
+        eref = O.corutv_lowrank_error(a, ref)
+        assert abs(err - eref) <= 1e-10 * np.linalg.norm(a)
+
+
+def test_rank_one_and_exactly_rank_deficient():
+    rng = np.random.Generator(np.random.PCG64(44))
+    a = np.outer(rng.standard_normal(500), rng.standard_normal(300))
+    f = P.corutv(a, P.SketchConfig(ell=10, q_power=1, seed=2))
+    assert np.linalg.norm(a - f.lowrank()) <= 1e-12 * np.linalg.norm(a)
+    d = np.abs(np.diag(f.t))
+    assert d[0] > 0 and np.all(d[1:] <= 1e-12 * d[0])
+    assert np.all(np.isfinite(f.u)) and np.all(np.isfinite(f.v))
