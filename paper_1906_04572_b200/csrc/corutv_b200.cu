@@ -55,6 +55,7 @@ struct corutv_handle {
   // of (index, u1, sign) come back with the counts in one readback
   unsigned char* tails = nullptr;
   int tails_cap = 0;
+  cudaEvent_t est_ev = nullptr;  // spectral norm: readiness of the async estimate
   // profiling (corutv_profile_begin/end): launch counter always on; CUDA
   // events around the DMMA GEMM / low-rank kernels while enabled.
   int64_t launches = 0;
@@ -1421,13 +1422,12 @@ void spectral_norm(corutv_handle* h, const double* a, int64_t m, int64_t n, int6
     if (sharded) allreduce(h, G, (int64_t)b * ldb2);
     small::sym_lmax_kernel<<<1, 32, 0, h->stream>>>(G, b, ldb2, sig);
     CK_LAUNCH();
-    CK(cudaMemcpyAsync(h->pinned, sig, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-    sync(h);
-    const double est = std::sqrt(std::max(h->pinned[0], 0.0));
-    if (iters) *iters = it + 1;
-    if (est == 0.0) { *out = 0.0; return; }
-    if (std::fabs(est - prev) <= 0.02 * tol * est) { *out = est; return; }
-    prev = est;
+    // the estimate comes back asynchronously: the next product and its QR
+    // are queued before the host looks at it (their synchronisations make it
+    // available); on convergence that speculative work is simply dropped,
+    // so the returned estimate and iteration count are the reference's
+    CK(cudaMemcpyAsync(h->pinned + 8, sig, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaEventRecord(h->est_ev, h->stream));
     // v = orth(A'^T w)
     if (tall) {
       run_gemm(h, true, n, b, m, A, ldA, w, ldb2, z0, ldb2, nullptr, 0, ws);
@@ -1437,6 +1437,12 @@ void spectral_norm(corutv_handle* h, const double* a, int64_t m, int64_t n, int6
       run_gemm(h, false, m, b, n, A, ldA, wT, round_up(mp, 16), z0, ldb2, nullptr, 0, ws);
     }
     double* q = cholqr(h, z0, z1, np, b, ldb2, (double)np, false, qw);
+    CK(cudaEventSynchronize(h->est_ev));
+    const double est = std::sqrt(std::max(h->pinned[8], 0.0));
+    if (iters) *iters = it + 1;
+    if (est == 0.0) { *out = 0.0; return; }
+    if (std::fabs(est - prev) <= 0.02 * tol * est) { *out = est; return; }
+    prev = est;
     if (q != v) CK(cudaMemcpyAsync(v, q, (size_t)np * ldb2 * 8, cudaMemcpyDeviceToDevice, h->stream));
     transpose(h, v, np, b, ldb2, vT, ldnp);
   }
@@ -1480,6 +1486,12 @@ int corutv_create(int device, void* stream, corutv_handle** out) {
     return CORUTV_ERR_NOMEM;
   }
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaEventCreateWithFlags(&h->est_ev, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFreeHost(h->pinned);
+    delete h;
+    return CORUTV_ERR_CUDA;
+  }
   // nested workspaces (e.g. the Gaussian generator inside a decomposition)
   // come from the device's default stream-ordered pool; keep its memory
   // mapped across synchronisations, or every call re-maps it (measured:
@@ -1504,6 +1516,7 @@ void corutv_destroy(corutv_handle* h) {
   for (cudaEvent_t e : h->chunk_ev) cudaEventDestroy(e);
   if (h->staging) cudaFreeHost(h->staging);
   if (h->tails) cudaFreeHost(h->tails);
+  if (h->est_ev) cudaEventDestroy(h->est_ev);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   delete h;
 }
