@@ -364,6 +364,19 @@ __global__ void __launch_bounds__(THREADS, 2)
   const int ncol0 = n0 + wn * 8 * J;
   const int nvf = max(0, min(J, (t.N - ncol0 + 7) / 8));
   const int mvf = max(0, min(4, (t.M - (m0 + wm * 32) + 7) / 8));
+  if (MODE != LR_STORE) {
+    // pull this tile's M (and Y) rows into L2 while the mainloop runs, so
+    // the streaming epilogue finds them there (128-byte lines, no registers)
+    const int tn = 16 * J;
+    const int lines_per_row = (tn * 8 + 127) / 128;
+    for (int e = threadIdx.x; e < BM * lines_per_row; e += THREADS) {
+      const int row = e / lines_per_row, ln = e % lines_per_row;
+      if (m0 + row >= t.M || n0 + ln * 16 >= t.N) continue;
+      const int64_t off = (int64_t)(m0 + row) * p.ld + n0 + ln * 16;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(p.m_mat + off));
+      if (MODE == LR_ALM) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.y + off));
+    }
+  }
   Acc<J> acc;
   acc.zero();
   bool bad = false;
