@@ -51,7 +51,8 @@ def check_factors(f, a, ell, tol=1e-10):
 @pytest.mark.parametrize("shape", [(1, 1, 1), (7, 3, 5), (130, 15, 33), (1000, 15, 1000),
                                    (4000, 50, 3000), (520, 110, 700), (300, 272, 513),
                                    (64, 600, 200), (257, 129, 4097), (96, 16, 64), (200, 32, 300),
-                                   (1000, 112, 800), (333, 80, 96)])
+                                   (1000, 112, 800), (333, 80, 96), (24, 24, 10000), (51, 51, 3000),
+                                   (64, 40, 777), (5, 64, 31)])
 def test_gemm_matches_numpy(trans, shape):
     M, N, K = shape
     rng = np.random.Generator(np.random.PCG64(M * 7 + N + K))
