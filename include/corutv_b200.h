@@ -150,6 +150,21 @@ int corutv_decompose_stream(corutv_handle* h, corutv_read_rows_fn read_rows, voi
                             int variant, const double* omega, const uint64_t* pcg_state,
                             double* u, double* t, double* v, int64_t* perm, int64_t* passes_host);
 
+/* sor_svd / tsr_svd of a HOST-resident A, streamed as corutv_decompose_host
+ * does: A (m x n, lda_host) is copied into a_dev (m x ld_dev, 16-byte
+ * aligned, ld_dev even) in row chunks overlapped with the first products
+ * (for tsr_svd both y = A psi and z = A' phi consume each chunk as it
+ * lands: one pass over the host data).  Bit-identical to the resident
+ * calls on a_dev. */
+int corutv_sor_svd_host(corutv_handle* h, const double* a_host, int64_t m, int64_t n, int64_t lda_host,
+                        double* a_dev, int64_t ld_dev, int ell, int q_power, int variant,
+                        const double* omega, const uint64_t* pcg_state, double* u, double* sigma,
+                        double* v, int64_t* passes_host);
+int corutv_tsr_svd_host(corutv_handle* h, const double* a_host, int64_t m, int64_t n, int64_t lda_host,
+                        double* a_dev, int64_t ld_dev, int ell, const double* psi,
+                        const uint64_t* pcg_psi, const double* phi, const uint64_t* pcg_phi,
+                        double* u, double* sigma, double* v, int64_t* passes_host);
+
 /* np.random.Generator(PCG64(seed)).standard_normal((rows, cols)) into out
  * (row-major, ld) on the device, bit-identical (gaussian_matrix,
  * sketch.py:63-68).  One stream synchronisation (tail-sample readback);

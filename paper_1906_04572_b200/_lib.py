@@ -44,6 +44,10 @@ SIGNATURES = {
     "corutv_gaussian": (_I32, [_VP, _VP, _I64, _I64, _VP, _I64]),
     "corutv_decompose_stream": (_I32, [_VP, READ_ROWS_FN, _VP, _I64, _I64, _VP, _I64, _I32, _I32, _I32, _VP,
                                        _VP, _VP, _VP, _VP, _VP, c_int64_p]),
+    "corutv_sor_svd_host": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _I64, _I32, _I32, _I32, _VP, _VP, _VP,
+                                   _VP, _VP, c_int64_p]),
+    "corutv_tsr_svd_host": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _I64, _I32, _VP, _VP, _VP, _VP, _VP,
+                                   _VP, _VP, c_int64_p]),
     "corutv_jacobi_svd": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _VP, _VP]),
     "corutv_sor_svd": (_I32, [_VP, _VP, _I64, _I64, _I64, _I32, _I32, _I32, _VP, _VP, _VP, _VP, _VP,
                               c_int64_p]),

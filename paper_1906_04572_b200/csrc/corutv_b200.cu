@@ -866,6 +866,72 @@ struct HostFeed {
   void* user = nullptr;
 };
 
+// Row-chunked H2D of a HostFeed into its device buffer (ld = lda) on the
+// handle's copy stream, one event per chunk; chunk 0 is queued by start().
+struct Feeder {
+  corutv_handle* h;
+  const HostFeed* feed;
+  int64_t m, n, lda;
+  int64_t chunk_rows = 0, n_chunks = 0;
+  int64_t row0(int64_t c) const { return c * chunk_rows; }
+  int64_t rows(int64_t c) const { return std::min(chunk_rows, m - c * chunk_rows); }
+  void start() {
+    if (!h->copy_stream) CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+    // ~1 GiB chunks (multiples of the 128-row tile); CORUTV_HOST_CHUNK_BYTES
+    // overrides the size (tests use small chunks)
+    int64_t chunk_bytes = (int64_t)1 << 30;
+    if (const char* env = std::getenv("CORUTV_HOST_CHUNK_BYTES")) chunk_bytes = std::max<int64_t>(1, std::atoll(env));
+    chunk_rows = std::max<int64_t>(gemm::BM, chunk_bytes / (8 * n) / gemm::BM * gemm::BM);
+    chunk_rows = std::min(chunk_rows, m);
+    n_chunks = (m + chunk_rows - 1) / chunk_rows;
+    if (feed->read_rows) {
+      const size_t need = (size_t)chunk_rows * n * 8;
+      if (h->staging_bytes < need) {
+        if (h->staging) CK(cudaFreeHost(h->staging));
+        h->staging = nullptr;
+        h->staging_bytes = 0;
+        if (cudaMallocHost(&h->staging, 2 * need) != cudaSuccess) {
+          cudaGetLastError();
+          fail(h, CORUTV_ERR_NOMEM, "pinned staging allocation failed");
+        }
+        h->staging_bytes = need;
+      }
+    }
+    while ((int64_t)h->chunk_ev.size() < n_chunks) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      h->chunk_ev.push_back(e);
+    }
+    // the buffer may be recycled memory: order the copies after the work
+    // already queued on the compute stream
+    CK(cudaEventRecord(h->chunk_ev[0], h->stream));
+    CK(cudaStreamWaitEvent(h->copy_stream, h->chunk_ev[0], 0));
+    enqueue(0);
+  }
+  void enqueue(int64_t c) {
+    const int64_t r0 = row0(c), nr = rows(c);
+    const double* src = feed->a_host + r0 * feed->ld_host;
+    int64_t ld_src = feed->ld_host;
+    if (feed->read_rows) {
+      // staging slot c % 2 was last used by chunk c - 2: wait for its copy
+      double* slot = h->staging + (size_t)(c & 1) * (h->staging_bytes / 8);
+      if (c >= 2) CK(cudaEventSynchronize(h->chunk_ev[c - 2]));
+      if (feed->read_rows(feed->user, r0, nr, slot, n) != 0)
+        fail(h, CORUTV_ERR_IO, "row reader failed at rows " + std::to_string(r0) + ".." + std::to_string(r0 + nr));
+      src = slot;
+      ld_src = n;
+    }
+    CK(cudaMemcpy2DAsync(feed->a_dev + r0 * lda, (size_t)lda * 8, src, (size_t)ld_src * 8, (size_t)n * 8,
+                         (size_t)nr, cudaMemcpyHostToDevice, h->copy_stream));
+    CK(cudaEventRecord(h->chunk_ev[c], h->copy_stream));
+  }
+  // queue the next chunk's copy, then make the compute stream wait for c
+  void next(int64_t c) {
+    if (c + 1 < n_chunks) enqueue(c + 1);
+    CK(cudaStreamWaitEvent(h->stream, h->chunk_ev[c], 0));
+  }
+};
+
 void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, int ell, int q,
                int variant, const double* omega, const uint64_t* pcg, double* u, double* t, double* v,
                int64_t* perm, int64_t* passes_host, double delta = -1.0, int* r_host = nullptr,
@@ -934,57 +1000,10 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   ar.commit();
 
   // host input: start the chunked H2D copy before anything else
-  int64_t chunk_rows = 0, n_chunks = 0;
-  auto enqueue_chunk = [&](int64_t c) {
-    const int64_t r0 = c * chunk_rows, rows = std::min(chunk_rows, m - r0);
-    const double* src = feed->a_host + r0 * feed->ld_host;
-    int64_t ld_src = feed->ld_host;
-    if (feed->read_rows) {
-      // staging slot c % 2 was last used by chunk c - 2: wait for its copy
-      double* slot = h->staging + (size_t)(c & 1) * (h->staging_bytes / 8);
-      if (c >= 2) CK(cudaEventSynchronize(h->chunk_ev[c - 2]));
-      if (feed->read_rows(feed->user, r0, rows, slot, n) != 0)
-        fail(h, CORUTV_ERR_IO, "row reader failed at rows " + std::to_string(r0) + ".." + std::to_string(r0 + rows));
-      src = slot;
-      ld_src = n;
-    }
-    CK(cudaMemcpy2DAsync(feed->a_dev + r0 * lda, (size_t)lda * 8, src, (size_t)ld_src * 8, (size_t)n * 8,
-                         (size_t)rows, cudaMemcpyHostToDevice, h->copy_stream));
-    CK(cudaEventRecord(h->chunk_ev[c], h->copy_stream));
-  };
+  Feeder fd{h, feed, m, n, lda};
   if (feed) {
     if (!a_ok) fail(h, CORUTV_ERR_ARG, "device buffer for the host input must be 16-byte aligned, even ld");
-    if (!h->copy_stream) CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
-    // ~1 GiB chunks (multiples of the 128-row tile); CORUTV_HOST_CHUNK_BYTES
-    // overrides the size (tests use small chunks)
-    int64_t chunk_bytes = (int64_t)1 << 30;
-    if (const char* env = std::getenv("CORUTV_HOST_CHUNK_BYTES")) chunk_bytes = std::max<int64_t>(1, std::atoll(env));
-    chunk_rows = std::max<int64_t>(gemm::BM, chunk_bytes / (8 * n) / gemm::BM * gemm::BM);
-    chunk_rows = std::min(chunk_rows, m);
-    n_chunks = (m + chunk_rows - 1) / chunk_rows;
-    if (feed->read_rows) {
-      const size_t need = (size_t)chunk_rows * n * 8;
-      if (h->staging_bytes < need) {
-        if (h->staging) CK(cudaFreeHost(h->staging));
-        h->staging = nullptr;
-        h->staging_bytes = 0;
-        if (cudaMallocHost(&h->staging, 2 * need) != cudaSuccess) {
-          cudaGetLastError();
-          fail(h, CORUTV_ERR_NOMEM, "pinned staging allocation failed");
-        }
-        h->staging_bytes = need;
-      }
-    }
-    while ((int64_t)h->chunk_ev.size() < n_chunks) {
-      cudaEvent_t e;
-      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      h->chunk_ev.push_back(e);
-    }
-    // the buffer may be recycled memory: order the copies after the work
-    // already queued on the compute stream
-    CK(cudaEventRecord(h->chunk_ev[0], h->stream));
-    CK(cudaStreamWaitEvent(h->copy_stream, h->chunk_ev[0], 0));
-    enqueue_chunk(0);
+    fd.start();
   }
   const double* A = a;
   if (!a_ok) {
@@ -1011,10 +1030,9 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
       const GemmPlan full = plan_gemm(h, m, l, n, true);
       const int64_t split_rows = (int64_t)k2plan.kps * gemm::BK;
       int next_split = 0;
-      for (int64_t c = 0; c < n_chunks; ++c) {
-        if (c + 1 < n_chunks) enqueue_chunk(c + 1);
-        CK(cudaStreamWaitEvent(h->stream, h->chunk_ev[c], 0));
-        const int64_t r0 = c * chunk_rows, rows = std::min(chunk_rows, m - r0);
+      for (int64_t c = 0; c < fd.n_chunks; ++c) {
+        fd.next(c);
+        const int64_t r0 = fd.row0(c), rows = fd.rows(c);
         run_gemm(h, false, rows, l, n, A + r0 * ldA, ldA, XT, ldn, C1a + r0 * ldp, ldp, nullptr, 0, ws, flag,
                  &full);
         while (ws2 && next_split < k2plan.splits &&
@@ -1134,7 +1152,7 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
 // FP64-tensor-bound for l >= ~25, so fusing them would not shorten the pass.
 void tsr(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, int ell, const double* psi,
          const uint64_t* pcg_psi, const double* phi, const uint64_t* pcg_phi, double* u, double* sigma, double* v,
-         int64_t* passes_host) {
+         int64_t* passes_host, const HostFeed* feed = nullptr) {
   if (!a || !u || !sigma || !v || (!psi && !pcg_psi) || (!phi && !pcg_phi))
     fail(h, CORUTV_ERR_ARG, "null pointer argument");
   if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
@@ -1173,7 +1191,16 @@ void tsr(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, i
   ar.add(&flag, 4);
   ar.add(&jstat, 4);
   ar.add(&info, 4);
+  // host input: z = A' phi split-K slices as the row chunks land
+  const GemmPlan zplan = plan_gemm(h, n, l, m, true);
+  double* ws2 = nullptr;
+  if (feed && zplan.splits > 1) ar.add(&ws2, (size_t)zplan.splits * n * round_up(l, 2) + 16);
   ar.commit();
+  Feeder fd{h, feed, m, n, lda};
+  if (feed) {
+    if (!a_ok) fail(h, CORUTV_ERR_ARG, "device buffer for the host input must be 16-byte aligned, even ld");
+    fd.start();
+  }
   const double* A = a;
   if (!a_ok) {
     copy2d(h, a, m, n, lda, Apad, ldA);
@@ -1188,7 +1215,27 @@ void tsr(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, i
   }
   if (phi) copy2d(h, phi, m, l, l, Phi, ldp);
   else gaussian(h, pcg_phi, m, l, Phi, ldp, nullptr, 0);
-  {
+  if (feed) {
+    // one pass over the host data: each row chunk feeds y = A psi (its rows,
+    // the full GEMM's split-K plan) and the split-K slices of z = A' phi
+    // whose rows it completes -- bit-identical to the resident products
+    TagScope ts(h, 1);
+    const GemmPlan yplan = plan_gemm(h, m, l, n, true);
+    const int64_t split_rows = (int64_t)zplan.kps * gemm::BK;
+    int next_split = 0;
+    for (int64_t c = 0; c < fd.n_chunks; ++c) {
+      fd.next(c);
+      const int64_t r0 = fd.row0(c), rows = fd.rows(c);
+      run_gemm(h, false, rows, l, n, A + r0 * ldA, ldA, PsiT, ldn, Y + r0 * ldp, ldp, nullptr, 0, ws, flag, &yplan);
+      while (ws2 && next_split < zplan.splits &&
+             r0 + rows >= std::min<int64_t>(m, (int64_t)(next_split + 1) * split_rows)) {
+        run_gemm_mm_split(h, zplan, n, l, m, A, ldA, Phi, ldp, ws2, next_split);
+        ++next_split;
+      }
+    }
+    if (ws2) finalize_splits(h, zplan, n, l, ws2, Z, ldp, nullptr, 0);
+    else run_gemm(h, true, n, l, m, A, ldA, Phi, ldp, Z, ldp, nullptr, 0, ws);
+  } else {
     TagScope ts(h, 1);
     run_gemm(h, false, m, l, n, A, ldA, PsiT, ldn, Y, ldp, nullptr, 0, ws, flag);  // y = A psi
     run_gemm(h, true, n, l, m, A, ldA, Phi, ldp, Z, ldp, nullptr, 0, ws);          // z = A' phi
@@ -1640,6 +1687,43 @@ int corutv_sor_svd(corutv_handle* hh, const double* a, int64_t m, int64_t n, int
   }
   decompose(h, a, m, n, lda, ell, q_power, variant, omega, omega ? nullptr : st, u, nullptr, v, nullptr,
             passes_host, -1.0, nullptr, nullptr, sigma);
+  ABI_END
+}
+
+int corutv_sor_svd_host(corutv_handle* hh, const double* a_host, int64_t m, int64_t n, int64_t lda_host,
+                        double* a_dev, int64_t ld_dev, int ell, int q_power, int variant, const double* omega,
+                        const uint64_t* pcg_state, double* u, double* sigma, double* v, int64_t* passes_host) {
+  ABI_BEGIN(hh)
+  if (!a_host || !a_dev || !sigma) fail(h, CORUTV_ERR_ARG, "null pointer argument");
+  if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
+  if (lda_host < n || ld_dev < n) fail(h, CORUTV_ERR_ARG, "leading dimension < n");
+  uint64_t st[4] = {0, 0, 0, 0};
+  if (!omega) {
+    if (!pcg_state) fail(h, CORUTV_ERR_ARG, "need omega or pcg_state");
+    for (int i = 0; i < 4; ++i) st[i] = pcg_state[i];
+  }
+  HostFeed feed{a_host, lda_host, a_dev};
+  decompose(h, a_dev, m, n, ld_dev, ell, q_power, variant, omega, omega ? nullptr : st, u, nullptr, v, nullptr,
+            passes_host, -1.0, nullptr, &feed, sigma);
+  ABI_END
+}
+
+int corutv_tsr_svd_host(corutv_handle* hh, const double* a_host, int64_t m, int64_t n, int64_t lda_host,
+                        double* a_dev, int64_t ld_dev, int ell, const double* psi, const uint64_t* pcg_psi,
+                        const double* phi, const uint64_t* pcg_phi, double* u, double* sigma, double* v,
+                        int64_t* passes_host) {
+  ABI_BEGIN(hh)
+  if (!a_host || !a_dev) fail(h, CORUTV_ERR_ARG, "null pointer argument");
+  if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
+  if (lda_host < n || ld_dev < n) fail(h, CORUTV_ERR_ARG, "leading dimension < n");
+  uint64_t s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0};
+  if (pcg_psi)
+    for (int i = 0; i < 4; ++i) s1[i] = pcg_psi[i];
+  if (pcg_phi)
+    for (int i = 0; i < 4; ++i) s2[i] = pcg_phi[i];
+  HostFeed feed{a_host, lda_host, a_dev};
+  tsr(h, a_dev, m, n, ld_dev, ell, psi, pcg_psi ? s1 : nullptr, phi, pcg_phi ? s2 : nullptr, u, sigma, v,
+      passes_host, &feed);
   ABI_END
 }
 

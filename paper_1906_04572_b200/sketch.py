@@ -203,6 +203,30 @@ def corutv(a, cfg: SketchConfig, counter: PassCounter | None = None, omega=None)
                          variant=cfg.variant, perm=dev.to_output(perm, was_host))
 
 
+def _host_source(a):
+    """(keep-alive source, host pointer, ld, output kind) of a host matrix:
+    numpy arrays come back as numpy, host torch tensors as host tensors."""
+    torch = dev.torch_mod()
+    if dev.is_host_tensor(a):
+        src = a if (a.dtype == torch.float64 and a.stride(1) == 1) else a.to(torch.float64).contiguous()
+        return src, src.data_ptr(), src.stride(0), "torch"
+    src = np.ascontiguousarray(a, dtype=np.float64)
+    return src, src.ctypes.data, src.shape[1], True
+
+
+def _staged_outputs(tensors, kind, device):
+    """D2H through pinned staging (torch's host caching allocator recycles
+    the blocks call to call), one synchronisation."""
+    torch = dev.torch_mod()
+    outs = []
+    for x in tensors:
+        y = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+        y.copy_(x, non_blocking=True)
+        outs.append(y)
+    torch.cuda.current_stream(device).synchronize()
+    return [y.numpy() for y in outs] if kind is True else outs
+
+
 def _corutv_host(a, cfg: SketchConfig, counter: PassCounter | None, omega) -> CorUtvFactors:
     """corutv of a host-resident matrix: the library streams A into a device
     buffer in row chunks and overlaps the copy with Omega and the first
@@ -210,12 +234,7 @@ def _corutv_host(a, cfg: SketchConfig, counter: PassCounter | None, omega) -> Co
     device-resident call.  Factors come back as numpy arrays (host torch
     tensors for a host torch input)."""
     torch = dev.torch_mod()
-    if dev.is_host_tensor(a):
-        src = a if (a.dtype == torch.float64 and a.stride(1) == 1) else a.to(torch.float64).contiguous()
-        host_ptr, ld_host, kind = src.data_ptr(), src.stride(0), "torch"
-    else:
-        src = np.ascontiguousarray(a, dtype=np.float64)
-        host_ptr, ld_host, kind = src.ctypes.data, src.shape[1], True
+    src, host_ptr, ld_host, kind = _host_source(a)
     m, n = src.shape
     ell = cfg.ell
     device = torch.device("cuda", torch.cuda.current_device())
@@ -235,16 +254,7 @@ def _corutv_host(a, cfg: SketchConfig, counter: PassCounter | None, omega) -> Co
     del src
     if counter is not None:
         counter.add(passes.value)
-    # factors come back through pinned staging (torch's host caching
-    # allocator recycles the blocks call to call)
-    outs = []
-    for x in (u, t, v, perm):
-        y = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
-        y.copy_(x, non_blocking=True)
-        outs.append(y)
-    torch.cuda.current_stream(device).synchronize()
-    if kind is True:
-        outs = [y.numpy() for y in outs]
+    outs = _staged_outputs((u, t, v, perm), kind, device)
     return CorUtvFactors(u=outs[0], t=outs[1], v=outs[2], ell=ell, q_power=cfg.q_power, variant=cfg.variant,
                          perm=outs[3])
 
@@ -278,19 +288,58 @@ def _svd_outputs(u, sigma, v, was_host):
                       v=dev.to_output(v, was_host))
 
 
+def _svd_host(kind_name, a, cfg, counter, g1, g2) -> SvdFactors:
+    """sor_svd / tsr_svd of a host matrix, streamed (corutv_{sor,tsr}_svd_host)."""
+    torch = dev.torch_mod()
+    src, host_ptr, ld_host, kind = _host_source(a)
+    m, n = src.shape
+    ell = cfg.ell
+    device = torch.device("cuda", torch.cuda.current_device())
+    ld_dev = n + (n & 1)
+    a_dev = torch.empty((m, ld_dev), dtype=torch.float64, device=device)
+    u = torch.empty((m, ell), dtype=torch.float64, device=device)
+    s = torch.empty((ell,), dtype=torch.float64, device=device)
+    v = torch.empty((n, ell), dtype=torch.float64, device=device)
+    passes = ctypes.c_int64(0)
+    h = _lib.handle(device.index)
+    if kind_name == "sor":
+        om = None if g1 is None else _omega_device(g1, n, ell, cfg.seed, a_dev)
+        h.call("corutv_sor_svd_host", host_ptr, m, n, ld_host, dev.ptr(a_dev), ld_dev, ell, cfg.q_power,
+               _VARIANT_CODE[cfg.variant], None if om is None else dev.ptr(om),
+               None if om is not None else pcg_state(cfg.seed), dev.ptr(u), dev.ptr(s), dev.ptr(v),
+               ctypes.byref(passes))
+    else:
+        ps = None if g1 is None else _omega_device(g1, n, ell, cfg.seed, a_dev)
+        ph = None if g2 is None else _omega_device(g2, m, ell, cfg.seed, a_dev)
+        h.call("corutv_tsr_svd_host", host_ptr, m, n, ld_host, dev.ptr(a_dev), ld_dev, ell,
+               None if ps is None else dev.ptr(ps), None if ps is not None else pcg_state(cfg.seed),
+               None if ph is None else dev.ptr(ph),
+               None if ph is not None else pcg_state((cfg.seed + SECOND_STREAM_OFFSET) % 2 ** 64),
+               dev.ptr(u), dev.ptr(s), dev.ptr(v), ctypes.byref(passes))
+    del src
+    if counter is not None:
+        counter.add(passes.value)
+    outs = _staged_outputs((u, s, v), kind, device)
+    return SvdFactors(u=outs[0], sigma=outs[1], v=outs[2])
+
+
 def sor_svd(a, cfg: SketchConfig, counter: PassCounter | None = None, omega=None) -> SvdFactors:
     """sketch.py:244-262: the corutv pipeline finished by a Jacobi SVD of the
     compressed core (corutv_sor_svd)."""
     torch = dev.torch_mod()
-    A, was_host = dev.to_device(a, "a")
-    m, n = A.shape
+    a = dev.shape_check(a, "a")
+    m, n = tuple(a.shape)
     if m < n or cfg.ell > min(m, n):
         # reference order: as_matrix's finiteness check comes first (dense.py:48);
         # otherwise the first sweep flags non-finite entries on the device
-        dev.raise_if_nonfinite(A, "a")
+        t_, _ = dev.to_device(a, "a")
+        dev.raise_if_nonfinite(t_, "a")
         if m < n:
             raise ValueError(f"sor_svd requires rows >= cols, got {m}x{n}")
         cfg.validated_for(m, n)
+    if not dev.is_device_tensor(a):
+        return _svd_host("sor", a, cfg, counter, omega, None)
+    A, was_host = dev.to_device(a, "a")
     ell = cfg.ell
     u = torch.empty((m, ell), dtype=torch.float64, device=A.device)
     s = torch.empty((ell,), dtype=torch.float64, device=A.device)
@@ -312,11 +361,15 @@ def tsr_svd(a, cfg: SketchConfig, counter: PassCounter | None = None, psi=None, 
     (corutv_tsr_svd).  One algorithmic pass (counted as the reference's
     fused sweep)."""
     torch = dev.torch_mod()
-    A, was_host = dev.to_device(a, "a")
-    m, n = A.shape
+    a = dev.shape_check(a, "a")
+    m, n = tuple(a.shape)
     if cfg.ell > min(m, n):
-        dev.raise_if_nonfinite(A, "a")  # reference order (dense.py:48)
+        t_, _ = dev.to_device(a, "a")
+        dev.raise_if_nonfinite(t_, "a")  # reference order (dense.py:48)
         cfg.validated_for(m, n)
+    if not dev.is_device_tensor(a):
+        return _svd_host("tsr", a, cfg, counter, psi, phi)
+    A, was_host = dev.to_device(a, "a")
     ell = cfg.ell
     u = torch.empty((m, ell), dtype=torch.float64, device=A.device)
     s = torch.empty((ell,), dtype=torch.float64, device=A.device)

@@ -116,3 +116,24 @@ def test_svd_sketch_validation():
     a[3, 4] = np.inf
     with pytest.raises(ValueError, match="non-finite"):
         P.tsr_svd(a, P.SketchConfig(ell=5))
+
+
+@pytest.mark.parametrize("chunk_bytes", [None, 300000])
+def test_svd_sketches_host_streamed_are_bitwise_device(monkeypatch, chunk_bytes):
+    """Host inputs stream through corutv_{sor,tsr}_svd_host (tsr: both
+    products consume each row chunk) -- bit-identical to the device calls."""
+    if chunk_bytes is not None:
+        monkeypatch.setenv("CORUTV_HOST_CHUNK_BYTES", str(chunk_bytes))
+    rng = np.random.Generator(np.random.PCG64(17))
+    a = rng.standard_normal((2500, 12)) @ rng.standard_normal((12, 430)) + 1e-4 * rng.standard_normal((2500, 430))
+    ad = torch.from_numpy(a).cuda()
+    for fn, cfg in ((P.sor_svd, P.SketchConfig(ell=20, q_power=1, seed=3)),
+                    (P.sor_svd, P.SketchConfig(ell=20, q_power=0, seed=3, variant=P.VARIANT_APPROX)),
+                    (P.tsr_svd, P.SketchConfig(ell=20, seed=3))):
+        cnt = P.PassCounter()
+        fh = fn(a, cfg, cnt)
+        fd = fn(ad, cfg)
+        assert isinstance(fh.u, np.ndarray)
+        assert cnt.passes == (1 if fn is P.tsr_svd else 2 * (cfg.q_power + 1) + (cfg.variant == P.VARIANT_EXACT))
+        for x, y in ((fh.u, fd.u), (fh.sigma, fd.sigma), (fh.v, fd.v)):
+            assert np.array_equal(x, y.cpu().numpy())
