@@ -294,7 +294,7 @@ GemmPlan plan_gemm(const corutv_handle* h, int64_t M, int64_t N, int64_t K, bool
   const int sms = h->num_sms;
   int best = 1;
   double best_cost = 1e300;
-  const int smax = allow_split ? std::min(64, std::max(1, p.k_tiles / 4)) : 1;
+  const int smax = allow_split ? std::min(2 * sms, std::max(1, p.k_tiles / 4)) : 1;
   for (int s = 1; s <= smax; ++s) {
     const int kps = (p.k_tiles + s - 1) / s;
     const int sa = (p.k_tiles + kps - 1) / kps;
