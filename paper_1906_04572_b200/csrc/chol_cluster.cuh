@@ -1,17 +1,20 @@
-// Cluster-parallel adaptive Cholesky step for large cores (l > 113, where
-// [G | I] no longer fits one CTA's shared memory).  Same algorithm as
-// chol_factor_kernel (small.cuh): blocked Cholesky of the augmented matrix
+// Cluster-parallel adaptive Cholesky step for cores l >= 64 (the one-CTA
+// kernel in small.cuh handles smaller ones).  Same algorithm as
+// chol_factor_kernel: blocked Cholesky of the augmented matrix
 // [G (+ sI) | I], whose right half becomes R^-T (= the Bt operand of the
 // X * R^-1 GEMM).  The matrix lives in L2-resident global scratch; a
-// thread-block cluster of CS CTAs shares every panel step:
-//   (a) every CTA's warp 0 factors the 32 x 32 diagonal block redundantly
-//       in registers (identical inputs -> identical result, so no flag or
-//       factor needs to cross CTAs); rank 0 writes it back;
-//   (b) the panel's forward substitution is split over all cluster threads;
-//   (c) each CTA stages the panel rows in its shared memory and updates its
-//       share of the trailing 4 x 4 tiles.
-// Two cluster barriers per 32-row panel.  kappa_F sums are reduced across
-// the cluster through DSMEM in rank order (deterministic).
+// thread-block cluster of CS CTAs shares every 32-row panel:
+//   (a) the diagonal block is factored redundantly in every CTA (identical
+//       inputs -> identical result, nothing crosses CTAs), one panel ahead:
+//       warp 0 updates and factors the next diagonal block while the other
+//       warps run the trailing update (lookahead);
+//   (b) the panel rows get R_kk^-T by forward substitution, a thread per
+//       column;
+//   (c) each CTA stages the panel with cp.async and the trailing Schur
+//       update runs as 32 x 32 DMMA tiles over all warps of the cluster.
+// Two cluster barriers per panel.  kappa_F sums are reduced across the
+// cluster through DSMEM in rank order (deterministic).  CHOL_PROF builds
+// print per-phase times (tools/ell600_probe.py with CORUTV_LIB).
 #pragma once
 #include <cooperative_groups.h>
 
@@ -36,7 +39,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define CHOL_T(i)
 #endif
 
-// shared memory (doubles): R and R^-1 of the diagonal block (32 x 33 each)
+// shared memory (doubles): the diagonal block R_kk (32 x 33), 1/diag(R_kk),
 // and the 32 panel rows staged with a padded stride (stride % 16 == 8:
 // the 4 rows a DMMA fragment touches fall on different bank halves)
 __host__ __device__ inline int stage_stride(int l) { return (l + 15) / 16 * 16 + 8; }
