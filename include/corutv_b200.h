@@ -165,6 +165,13 @@ int corutv_tsr_svd_host(corutv_handle* h, const double* a_host, int64_t m, int64
                         const uint64_t* pcg_psi, const double* phi, const uint64_t* pcg_phi,
                         double* u, double* sigma, double* v, int64_t* passes_host);
 
+/* Host -> device copy of a row-major matrix (the as_matrix upload of a
+ * numpy input, dense.py:41-50) in ~1 GiB row chunks on the copy stream:
+ * pinned sources by DMA, pageable ones through pinned staging filled by a
+ * multi-threaded host copy.  Returns after the copy completed. */
+int corutv_upload(corutv_handle* h, const double* host, int64_t rows, int64_t cols, int64_t ld_host,
+                  double* dev, int64_t ld_dev);
+
 /* np.random.Generator(PCG64(seed)).standard_normal((rows, cols)) into out
  * (row-major, ld) on the device, bit-identical (gaussian_matrix,
  * sketch.py:63-68).  One stream synchronisation (tail-sample readback);

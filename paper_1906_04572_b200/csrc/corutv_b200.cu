@@ -1786,6 +1786,20 @@ int corutv_tsr_svd(corutv_handle* hh, const double* a, int64_t m, int64_t n, int
   ABI_END
 }
 
+int corutv_upload(corutv_handle* hh, const double* host, int64_t rows, int64_t cols, int64_t ld_host, double* dev,
+                  int64_t ld_dev) {
+  ABI_BEGIN(hh)
+  if (!host || !dev) fail(h, CORUTV_ERR_ARG, "null pointer argument");
+  if (rows < 1 || cols < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
+  if (ld_host < cols || ld_dev < cols) fail(h, CORUTV_ERR_ARG, "leading dimension < cols");
+  HostFeed feed{host, ld_host, dev};
+  Feeder fd{h, &feed, rows, cols, ld_dev};
+  fd.start();
+  for (int64_t c = 0; c < fd.n_chunks; ++c) fd.next(c);
+  sync(h);  // the caller may release the host buffer on return
+  ABI_END
+}
+
 int corutv_decompose_stream(corutv_handle* hh, corutv_read_rows_fn read_rows, void* user, int64_t m, int64_t n,
                             double* a_dev, int64_t ld_dev, int ell, int q_power, int variant, const double* omega,
                             const uint64_t* pcg_state, double* u, double* t, double* v, int64_t* perm,

@@ -621,3 +621,17 @@ def test_rank_one_and_exactly_rank_deficient():
     d = np.abs(np.diag(f.t))
     assert d[0] > 0 and np.all(d[1:] <= 1e-12 * d[0])
     assert np.all(np.isfinite(f.u)) and np.all(np.isfinite(f.v))
+
+
+@pytest.mark.parametrize("shape", [(3000, 3001), (9000, 1000)])
+def test_large_numpy_upload_is_exact(monkeypatch, shape):
+    """Numpy inputs above 64 MB go through corutv_upload (chunked, pinned
+    staging filled by host threads): the device copy is exact."""
+    from paper_1906_04572_b200 import _device
+
+    monkeypatch.setenv("CORUTV_HOST_CHUNK_BYTES", str(5 << 20))
+    a = np.random.Generator(np.random.PCG64(shape[1])).standard_normal(shape)
+    assert a.nbytes >= _device.UPLOAD_MIN_BYTES
+    t, was_host = _device.to_device(a, "a")
+    assert was_host is True and t.is_cuda
+    assert torch.equal(t, torch.from_numpy(a).cuda())
