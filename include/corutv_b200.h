@@ -172,6 +172,13 @@ int corutv_tsr_svd_host(corutv_handle* h, const double* a_host, int64_t m, int64
 int corutv_upload(corutv_handle* h, const double* host, int64_t rows, int64_t cols, int64_t ld_host,
                   double* dev, int64_t ld_dev);
 
+/* Device -> host copy of a row-major matrix (factors or L, S returned to a
+ * numpy caller) through two pinned staging slots: the D2H of one chunk
+ * overlaps the multi-threaded copy-out of the previous one.  Ordered after
+ * the work queued on the handle's stream; returns when the data is in host. */
+int corutv_download(corutv_handle* h, const double* dev, int64_t rows, int64_t cols, int64_t ld_dev,
+                    double* host, int64_t ld_host);
+
 /* np.random.Generator(PCG64(seed)).standard_normal((rows, cols)) into out
  * (row-major, ld) on the device, bit-identical (gaussian_matrix,
  * sketch.py:63-68).  One stream synchronisation (tail-sample readback);

@@ -49,6 +49,7 @@ SIGNATURES = {
     "corutv_tsr_svd_host": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _I64, _I32, _VP, _VP, _VP, _VP, _VP,
                                    _VP, _VP, c_int64_p]),
     "corutv_upload": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _I64]),
+    "corutv_download": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _I64]),
     "corutv_jacobi_svd": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _VP, _VP]),
     "corutv_sor_svd": (_I32, [_VP, _VP, _I64, _I64, _I64, _I32, _I32, _I32, _VP, _VP, _VP, _VP, _VP,
                               c_int64_p]),

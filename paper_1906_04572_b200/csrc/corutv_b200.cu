@@ -1800,6 +1800,53 @@ int corutv_upload(corutv_handle* hh, const double* host, int64_t rows, int64_t c
   ABI_END
 }
 
+int corutv_download(corutv_handle* hh, const double* dev, int64_t rows, int64_t cols, int64_t ld_dev, double* host,
+                    int64_t ld_host) {
+  ABI_BEGIN(hh)
+  if (!host || !dev) fail(h, CORUTV_ERR_ARG, "null pointer argument");
+  if (rows < 1 || cols < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
+  if (ld_host < cols || ld_dev < cols) fail(h, CORUTV_ERR_ARG, "leading dimension < cols");
+  if (!h->copy_stream) CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+  int64_t chunk_bytes = (int64_t)1 << 30;
+  if (const char* env = std::getenv("CORUTV_HOST_CHUNK_BYTES")) chunk_bytes = std::max<int64_t>(1, std::atoll(env));
+  const int64_t chunk_rows = std::min(rows, std::max<int64_t>(1, chunk_bytes / (8 * cols)));
+  const int64_t n_chunks = (rows + chunk_rows - 1) / chunk_rows;
+  const size_t need = (size_t)chunk_rows * cols * 8;
+  if (h->staging_bytes < need) {
+    if (h->staging) CK(cudaFreeHost(h->staging));
+    h->staging = nullptr;
+    h->staging_bytes = 0;
+    if (cudaMallocHost(&h->staging, 2 * need) != cudaSuccess) {
+      cudaGetLastError();
+      fail(h, CORUTV_ERR_NOMEM, "pinned staging allocation failed");
+    }
+    h->staging_bytes = need;
+  }
+  while ((int64_t)h->chunk_ev.size() < std::max<int64_t>(n_chunks, 1)) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    h->chunk_ev.push_back(e);
+  }
+  // the data is produced on the compute stream
+  CK(cudaEventRecord(h->chunk_ev[0], h->stream));
+  CK(cudaStreamWaitEvent(h->copy_stream, h->chunk_ev[0], 0));
+  auto slot = [&](int64_t c) { return h->staging + (size_t)(c & 1) * (h->staging_bytes / 8); };
+  auto nrows = [&](int64_t c) { return std::min(chunk_rows, rows - c * chunk_rows); };
+  // D2H of chunk c overlaps the host-side copy-out of chunk c - 1
+  for (int64_t c = 0; c <= n_chunks; ++c) {
+    if (c < n_chunks) {
+      CK(cudaMemcpy2DAsync(slot(c), (size_t)cols * 8, dev + c * chunk_rows * ld_dev, (size_t)ld_dev * 8,
+                           (size_t)cols * 8, (size_t)nrows(c), cudaMemcpyDeviceToHost, h->copy_stream));
+      CK(cudaEventRecord(h->chunk_ev[c], h->copy_stream));
+    }
+    if (c >= 1) {
+      CK(cudaEventSynchronize(h->chunk_ev[c - 1]));
+      parallel_copy_rows(host + (c - 1) * chunk_rows * ld_host, ld_host, slot(c - 1), cols, nrows(c - 1), cols);
+    }
+  }
+  ABI_END
+}
+
 int corutv_decompose_stream(corutv_handle* hh, corutv_read_rows_fn read_rows, void* user, int64_t m, int64_t n,
                             double* a_dev, int64_t ld_dev, int ell, int q_power, int variant, const double* omega,
                             const uint64_t* pcg_state, double* u, double* t, double* v, int64_t* perm,

@@ -635,3 +635,17 @@ def test_large_numpy_upload_is_exact(monkeypatch, shape):
     t, was_host = _device.to_device(a, "a")
     assert was_host is True and t.is_cuda
     assert torch.equal(t, torch.from_numpy(a).cuda())
+
+
+def test_large_output_download_is_exact(monkeypatch):
+    """Large numpy results (L, S) come back through corutv_download."""
+    from paper_1906_04572_b200 import _device
+
+    monkeypatch.setenv("CORUTV_HOST_CHUNK_BYTES", str(3 << 20))
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    t = torch.randn((5000, 2100), generator=g, dtype=torch.float64, device="cuda")
+    out = _device.to_output(t, True)
+    assert isinstance(out, np.ndarray) and np.array_equal(out, t.cpu().numpy())
+    view = t[:, :2000]  # strided view: the plain path
+    assert np.array_equal(_device.to_output(view, True), view.cpu().numpy())
