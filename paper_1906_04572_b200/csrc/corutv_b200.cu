@@ -277,16 +277,30 @@ struct GemmPlan {
 
 GemmPlan plan_gemm(const corutv_handle* h, int64_t M, int64_t N, int64_t K, bool allow_split) {
   GemmPlan p;
-  if (N <= 64) {
-    // narrow products (spectral-norm blocks, small ALM samples): 8-column
-    // granularity, e.g. N = 24 computes 24 columns instead of 32
-    p.WN = 1;
-    p.n_tiles = 1;
-    p.J = (int)std::max<int64_t>(1, (N + 7) / 8);
-  } else {
-    p.WN = 2;
-    p.n_tiles = (int)((N + 127) / 128);
-    p.J = (int)std::min<int64_t>(8, std::max<int64_t>(1, (N + 16 * p.n_tiles - 1) / (16 * p.n_tiles)));
+  // column tiling: CTA 128 x 16J (WN = 2) or 256 x 8J (WN = 1, 8-column
+  // granularity), J <= 8; pick the fewest padded columns (e.g. N = 24 -> 24
+  // not 32, N = 272 -> 280 not 288, N = 600 -> 616 not 640); ties go to
+  // WN = 1 for N <= 64 (narrow, memory-bound) and WN = 2 above, then to the
+  // fewest tiles
+  {
+    int64_t best_pad = INT64_MAX;
+    const int wn_first = N <= 64 ? 1 : 2;
+    for (int w = 0; w < 2; ++w) {
+      const int wn = w == 0 ? wn_first : 3 - wn_first;
+      const int64_t g = 8 * wn;  // columns per J
+      const int64_t nt_min = (N + 8 * g - 1) / (8 * g);
+      for (int64_t nt = nt_min; nt <= nt_min + 4; ++nt) {
+        const int64_t J = std::max<int64_t>(1, (N + g * nt - 1) / (g * nt));
+        if (J > 8) continue;
+        const int64_t pad = nt * g * J - N;
+        if (pad < best_pad) {
+          best_pad = pad;
+          p.WN = wn;
+          p.n_tiles = (int)nt;
+          p.J = (int)J;
+        }
+      }
+    }
   }
   const int bm = gemm::bm_of(p.WN);
   p.m_tiles = (int)((M + bm - 1) / bm);
@@ -399,12 +413,13 @@ void run_gemm(corutv_handle* h, bool mm, int64_t M, int64_t N, int64_t K, const 
   if (!mm) {
     ma = make_map(h, A, K, M, lda, bm);
     mb = make_map(h, B, K, N, ldb, bn);
-  } else if (make_map3d(h, A, M, K, lda, bm / 16, &ma) &&
-             make_map3d(h, B, N, K, ldb, gemm::nb16_of(p.J, p.WN), &mb)) {
-    t.mm3d = 1;
   } else {
-    ma = make_map(h, A, M, K, lda, gemm::BK);
-    mb = make_map(h, B, N, K, ldb, gemm::BK);
+    // 3-D boxes need the tile's first column on a 16-column group: always for
+    // A (bm is a multiple of 16), for B only when bn is (or one column tile)
+    if (make_map3d(h, A, M, K, lda, bm / 16, &ma)) t.mm3d |= 1;
+    else ma = make_map(h, A, M, K, lda, gemm::BK);
+    if ((bn % 16 == 0 || p.n_tiles == 1) && make_map3d(h, B, N, K, ldb, gemm::nb16_of(p.J, p.WN), &mb)) t.mm3d |= 2;
+    else mb = make_map(h, B, N, K, ldb, gemm::BK);
   }
   static const bool debug_plan = std::getenv("CORUTV_DEBUG_PLAN") != nullptr;
   if (debug_plan)

@@ -61,7 +61,7 @@ struct Tile {
   int k_tiles;          // total k tiles (ceil(K / 16))
   int k_tiles_per_split;
   int splits;
-  int mm3d;             // MM operands: one 3-D box per stage instead of 2-D boxes
+  int mm3d;             // MM operands as one 3-D box per stage: bit 0 A, bit 1 B
 };
 
 // Accumulator for one consumer warp: 4 (M) x J (N) DMMA fragments.
@@ -109,17 +109,24 @@ __device__ __forceinline__ void issue_stage(const Smem& sm, const CUtensorMap* m
   if (!MM) {
     tma_load_2d(sa, mapA, &sm.full[st], kt * BK, m0);
     tma_load_2d(sb, mapB, &sm.full[st], kt * BK, n0);
-  } else if (mm3d) {
-    // dims {16 cols, rows, column groups}: the box lands as [group][row][16]
-    tma_load_3d(sa, mapA, &sm.full[st], 0, kt * BK, m0 / 16);
-    tma_load_3d(sb, mapB, &sm.full[st], 0, kt * BK, n0 / 16);
   } else {
+    // mm3d bit 0 / bit 1: A / B fetched as one 3-D box {16 cols, rows, column
+    // groups} (lands as [group][row][16]); otherwise one 2-D box per 16
+    // columns (B columns need not start on a 16-column group)
+    if (mm3d & 1) {
+      tma_load_3d(sa, mapA, &sm.full[st], 0, kt * BK, m0 / 16);
+    } else {
 #pragma unroll
-    for (int bx = 0; bx < BMW / 16; ++bx)
-      tma_load_2d(sa + bx * 16 * BK, mapA, &sm.full[st], m0 + 16 * bx, kt * BK);
+      for (int bx = 0; bx < BMW / 16; ++bx)
+        tma_load_2d(sa + bx * 16 * BK, mapA, &sm.full[st], m0 + 16 * bx, kt * BK);
+    }
+    if (mm3d & 2) {
+      tma_load_3d(sb, mapB, &sm.full[st], 0, kt * BK, n0 / 16);
+    } else {
 #pragma unroll
-    for (int bx = 0; bx < NB16; ++bx)
-      tma_load_2d(sb + bx * 16 * BK, mapB, &sm.full[st], n0 + 16 * bx, kt * BK);
+      for (int bx = 0; bx < NB16; ++bx)
+        tma_load_2d(sb + bx * 16 * BK, mapB, &sm.full[st], n0 + 16 * bx, kt * BK);
+    }
   }
 }
 
