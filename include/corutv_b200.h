@@ -112,10 +112,30 @@ int corutv_decompose_host(corutv_handle* h, const double* a_host, int64_t m, int
 /* Economy SVD by one-sided Jacobi (dense.py:357-376, tol 1e-14, 100
  * sweeps; zero singular values get the deterministic orthonormal completion
  * of dense.py:285-310): u (m x k), sigma (k, descending), v (n x k), k =
- * min(m, n) <= 640, all device row-major.  CORUTV_ERR_CONVERGENCE if the
+ * min(m, n) <= 16384, all device row-major.  CORUTV_ERR_CONVERGENCE if the
  * sweeps do not converge. */
 int corutv_jacobi_svd(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda,
                       double* u, double* sigma, double* v);
+
+/* jacobi_svd(a, v_init=...) (dense.py:313-376 warm start): the sweeps start
+ * from A_tall v_init, A_tall = a (m >= n) or a' (m < n), and the right
+ * factor of A_tall is v_init times the rotations.  v_init: k x k device
+ * (ld ldvi), orthonormal; NULL = corutv_jacobi_svd.  Replaces
+ * _jacobi_svd_tall's v_init branch dense.py:315-321, 352-353. */
+int corutv_jacobi_svd_warm(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda,
+                           const double* v_init, int64_t ldvi, double* u, double* sigma,
+                           double* v);
+
+/* Singular value thresholding step of the InexactALM baseline
+ * (_svt_warm rpca.py:146-158): warm-started Jacobi SVD of b (m x n), then
+ * kept = max(sigma - delta, 0) (k), t = diag(kept) (k x k, ld k),
+ * *r_host = #(kept > 0), capped at `cap` when cap >= 0.  u (m x k), v
+ * (n x k) as corutv_jacobi_svd_warm, so u[:, :r] (t[:r, :] v') is the
+ * thresholded matrix (feed u, t, v, ell = k, r to corutv_alm_update /
+ * corutv_lowrank); v is the next call's v_init for square b. */
+int corutv_svt(corutv_handle* h, const double* b, int64_t m, int64_t n, int64_t ldb,
+               double delta, int cap, const double* v_init, int64_t ldvi, double* u,
+               double* kept, double* v, double* t, int* r_host);
 
 /* sor_svd (sketch.py:244-262): the corutv pipeline (power sketch, both
  * sketch QRs, exact or approximate compression) finished by a one-sided

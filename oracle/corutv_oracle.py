@@ -26,6 +26,7 @@ __all__ = [
     "pseudoinverse", "spectral_norm",
     "corutv", "corutv_lowrank_error", "flop_estimate", "sor_svd", "tsr_svd", "SECOND_STREAM_OFFSET",
     "shrink", "truncate_utv", "numerical_rank", "next_cap", "alm_corutv",
+    "svt", "svt_warm", "inexact_alm",
     "solver_flops",
 ]
 
@@ -216,12 +217,18 @@ def _jacobi_rotate(x, tol, max_sweeps, want_v):
         f"one-sided Jacobi did not converge in {max_sweeps} sweeps", residual=off)
 
 
-def _jacobi_tall(a, want_uv):
-    """dense.py:313-354 without warm start: QR-precondition when m > n, pad
-    odd widths with a zero column, sort descending (stable)."""
+def _jacobi_tall(a, want_uv, v_init=None):
+    """dense.py:313-354: warm start X = A v_init when given, else
+    QR-precondition when m > n; pad odd widths with a zero column, sort
+    descending (stable); V = v_init Vrot when warm-started."""
     m, n = a.shape
     q0 = None
-    if m > n:
+    if v_init is not None:
+        v_init = as_matrix(v_init, "v_init")
+        if v_init.shape != (n, n):
+            raise ValueError(f"v_init must be {n}x{n}, got {v_init.shape}")
+        x = np.asfortranarray(a @ v_init)
+    elif m > n:
         q0, x = householder_qr(a)
         x = np.asfortranarray(x)
     else:
@@ -246,7 +253,10 @@ def _jacobi_tall(a, want_uv):
         _complete_orthonormal(u, np.nonzero(~nz)[0])   # dense.py:347-349
     if q0 is not None:
         u = q0 @ u
-    return u, sig, vr[:, order]
+    v = vr[:, order]
+    if v_init is not None:
+        v = v_init @ v
+    return u, sig, v
 
 
 def jacobi_singular_values(a):
@@ -283,12 +293,12 @@ def _complete_orthonormal(u, fill):
         basis.append(w)
 
 
-def jacobi_svd(a):
-    """dense.py:357-376 (no warm start).  Returns (u, sigma, v)."""
+def jacobi_svd(a, v_init=None):
+    """dense.py:357-376.  Returns (u, sigma, v)."""
     a = as_matrix(a, "a")
     if a.shape[0] >= a.shape[1]:
-        return _jacobi_tall(a, True)
-    u, s, v = _jacobi_tall(a.T, True)
+        return _jacobi_tall(a, True, v_init)
+    u, s, v = _jacobi_tall(a.T, True, v_init)
     return v, s, u
 
 
@@ -467,11 +477,30 @@ def next_cap(cap, rank, limit, grow):
     return max(1, min(rank + grow, limit))
 
 
-def alm_corutv(m_mat, ell, lam=None, mu0=None, rho=1.5, mu_bar=None, tol=1e-5,
-               max_iter=1000, q_power=1, seed=0):
-    """rpca.py:175-255 (alm_corutv + _alm_loop).  Returns a dict with the
-    RpcaSolution fields (l, s, iterations, residuals, rank_of_l, nnz_of_s,
-    rank_history, nnz_history, mu_history, ell_history) plus ``mu0``."""
+def svt_warm(b, delta, v_init=None, cap=None):
+    """rpca.py:146-158 (_svt_warm): threshold the Jacobi spectrum of b.
+    Returns (matrix, r, v, kept[:r])."""
+    if delta < 0:
+        raise ValueError("delta must be >= 0")
+    b = as_matrix(b, "b")
+    u, sig, v = jacobi_svd(b, v_init)
+    kept = np.maximum(sig - delta, 0.0)
+    r = int((kept > 0.0).sum())
+    if cap is not None:
+        r = min(r, cap)
+    if r == 0:
+        return np.zeros_like(b), 0, v, np.zeros(0)
+    return (u[:, :r] * kept[:r]) @ v[:, :r].T, r, v, kept[:r]
+
+
+def svt(b, delta):
+    """rpca.py:135-143."""
+    mat, r, _, _ = svt_warm(b, delta)
+    return mat, r
+
+
+def _alm_loop(m_mat, step, cap0, lam=None, mu0=None, rho=1.5, mu_bar=None, tol=1e-5, max_iter=1000):
+    """rpca.py:175-234: step(g, delta, cap, j, state) -> (L, rank, sig, state)."""
     m_mat = as_matrix(m_mat, "m")
     h, w = m_mat.shape
     lam = lam if lam is not None else 1.0 / np.sqrt(max(h, w))
@@ -486,14 +515,14 @@ def alm_corutv(m_mat, ell, lam=None, mu0=None, rho=1.5, mu_bar=None, tol=1e-5,
     mu_bar = mu_bar if mu_bar is not None else 1e7 * mu
     limit = min(h, w)
     grow = max(1, round(0.05 * limit))
-    cap = max(1, min(ell, limit))
+    cap = max(1, min(cap0, limit))
     y = np.zeros_like(m_mat)
     s = np.zeros_like(m_mat)
     hist = dict(residuals=[], rank_history=[], nnz_history=[], mu_history=[],
                 ell_history=[])
+    state = None
     for j in range(max_iter):
-        f = corutv(m_mat - s + y / mu, cap, q_power, (seed + j) % 2 ** 64)
-        l, rank, sig = truncate_utv(f, 1.0 / mu)
+        l, rank, sig, state = step(m_mat - s + y / mu, 1.0 / mu, cap, j, state)
         hist["ell_history"].append(cap)
         cap = next_cap(cap, rank, limit, grow)
         g = m_mat - l + y / mu
@@ -513,6 +542,33 @@ def alm_corutv(m_mat, ell, lam=None, mu0=None, rho=1.5, mu_bar=None, tol=1e-5,
     raise OracleConvergenceError(
         f"ALM did not reach tol={tol:.1e} in {max_iter} iterations",
         residual=hist["residuals"][-1], history=hist["residuals"])
+
+
+def alm_corutv(m_mat, ell, lam=None, mu0=None, rho=1.5, mu_bar=None, tol=1e-5,
+               max_iter=1000, q_power=1, seed=0):
+    """rpca.py:237-255 (alm_corutv + _alm_loop).  Returns a dict with the
+    RpcaSolution fields (l, s, iterations, residuals, rank_of_l, nnz_of_s,
+    rank_history, nnz_history, mu_history, ell_history) plus ``mu0``."""
+
+    def step(g, delta, cap, j, state):
+        f = corutv(g, cap, q_power, (seed + j) % 2 ** 64)
+        l, rank, sig = truncate_utv(f, delta)
+        return l, rank, sig, None
+
+    return _alm_loop(m_mat, step, ell, lam, mu0, rho, mu_bar, tol, max_iter)
+
+
+def inexact_alm(m_mat, ell=None, lam=None, mu0=None, rho=1.5, mu_bar=None, tol=1e-5,
+                max_iter=1000):
+    """rpca.py:258-273: the same loop with the warm-started SVT step."""
+
+    def step(g, delta, cap, j, state):
+        mat, r, v, kept = svt_warm(g, delta, state, cap)
+        return mat, r, kept, v
+
+    m_arr = as_matrix(m_mat, "m")
+    cap0 = ell if ell is not None else min(m_arr.shape)
+    return _alm_loop(m_arr, step, cap0, lam, mu0, rho, mu_bar, tol, max_iter)
 
 
 def solver_flops(n, q_power, rank_history, ell_history):

@@ -8,13 +8,15 @@ include/corutv_b200.h).  There is no CPU fallback.
 
 :func:`install` rebinds the reference package's names to this
 implementation: ``corutv.sketch.corutv``, ``corutv.rpca.corutv``,
-``corutv.bench.corutv``, ``corutv.corutv``, ``corutv.rpca.alm_corutv`` and
-``corutv.alm_corutv``.
+``corutv.bench.corutv``, ``corutv.corutv``, ``corutv.rpca.alm_corutv``,
+``corutv.alm_corutv``, ``sor_svd`` / ``tsr_svd`` and the InexactALM baseline
+(``corutv.rpca.inexact_alm``, ``corutv.rpca.svt``).
 """
 
 from .dense import frobenius_norm, singular_values, spectral_norm
 from .errors import ConvergenceError, CorutvError
-from .rpca import AlmConfig, RpcaSolution, alm_corutv, corutv_threshold, shrink, write_telemetry_csv
+from .rpca import (AlmConfig, RpcaSolution, alm_corutv, corutv_threshold, inexact_alm, shrink, svt,
+                   write_telemetry_csv)
 from .sketch import (
     VARIANT_APPROX,
     VARIANT_EXACT,
@@ -30,7 +32,7 @@ from .sketch import (
     sor_svd,
     tsr_svd,
 )
-from .dense import SvdFactors
+from .dense import SvdFactors, jacobi_svd
 
 __version__ = "0.1.0"
 
@@ -39,7 +41,7 @@ __all__ = [
     "RpcaSolution", "SketchConfig", "VARIANT_APPROX", "VARIANT_EXACT", "alm_corutv", "corutv",
     "corutv_kpq", "corutv_lowrank_error", "corutv_threshold", "count_passes", "flop_estimate",
     "frobenius_norm", "gaussian_matrix", "install", "shrink", "singular_values", "spectral_norm",
-    "write_telemetry_csv", "sor_svd", "tsr_svd", "SvdFactors",
+    "write_telemetry_csv", "sor_svd", "tsr_svd", "SvdFactors", "inexact_alm", "svt", "jacobi_svd",
 ]
 
 
@@ -60,6 +62,9 @@ def install(ref_pkg=None):
         ("bench", "corutv", corutv),
         ("rpca", "alm_corutv", alm_corutv),
         ("bench", "alm_corutv", alm_corutv),
+        ("rpca", "inexact_alm", inexact_alm),
+        ("bench", "inexact_alm", inexact_alm),
+        ("rpca", "svt", svt),
     ):
         try:
             mod = importlib.import_module(f"{ref_pkg.__name__}.{modname}")
@@ -71,4 +76,8 @@ def install(ref_pkg=None):
     for name, obj in (("corutv", corutv), ("alm_corutv", alm_corutv)):
         setattr(ref_pkg, name, obj)
         done.append(f"{ref_pkg.__name__}.{name}")
+    for name, obj in (("sor_svd", sor_svd), ("tsr_svd", tsr_svd), ("inexact_alm", inexact_alm), ("svt", svt)):
+        if hasattr(ref_pkg, name):
+            setattr(ref_pkg, name, obj)
+            done.append(f"{ref_pkg.__name__}.{name}")
     return done

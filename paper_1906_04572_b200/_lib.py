@@ -51,6 +51,9 @@ SIGNATURES = {
     "corutv_upload": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _I64]),
     "corutv_download": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _I64]),
     "corutv_jacobi_svd": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _VP, _VP]),
+    "corutv_jacobi_svd_warm": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _I64, _VP, _VP, _VP]),
+    "corutv_svt": (_I32, [_VP, _VP, _I64, _I64, _I64, _D, _I32, _VP, _I64, _VP, _VP, _VP, _VP,
+                          ctypes.POINTER(_I32)]),
     "corutv_sor_svd": (_I32, [_VP, _VP, _I64, _I64, _I64, _I32, _I32, _I32, _VP, _VP, _VP, _VP, _VP,
                               c_int64_p]),
     "corutv_tsr_svd": (_I32, [_VP, _VP, _I64, _I64, _I64, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP,

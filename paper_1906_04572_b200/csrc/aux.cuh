@@ -169,4 +169,23 @@ __global__ void fill_kernel(double* p, int64_t n, double v) {
     p[idx] = v;
 }
 
+// Singular value threshold of sorted sigma (rpca.py:150-156):
+// kept = max(sigma - delta, 0), T = diag(kept) (k x k, ld ldt), *count +=
+// #(kept > 0).  T feeds the fused ALM update as the core of U T V'.
+__global__ void svt_kept_kernel(const double* sig, int k, double delta, double* kept, double* t, int64_t ldt,
+                                int* count) {
+  const int64_t total = (int64_t)k * k;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / k), j = (int)(idx % k);
+    double v = 0.0;
+    if (i == j) {
+      v = fmax(sig[i] - delta, 0.0);
+      kept[i] = v;
+      if (v > 0.0) atomicAdd(count, 1);
+    }
+    t[i * ldt + j] = v;
+  }
+}
+
 }  // namespace aux

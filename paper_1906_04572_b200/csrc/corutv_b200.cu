@@ -31,6 +31,7 @@
 #include "rng.cuh"
 #include "qrcp_cluster.cuh"
 #include "small.cuh"
+#include "jacobi_grid.cuh"
 
 #define CORUTV_VERSION 100
 
@@ -705,8 +706,55 @@ void qrcp(corutv_handle* h, const double* D, int l, int64_t ldd, double* T, int6
   ++h->launches;
 }
 
+// Grid-wide one-sided Jacobi (jacobi_grid.cuh) on a padded copy of X: the
+// cores that do not fit one CTA's shared memory.  status: device int, set
+// like the one-CTA kernel's (0 ok, 1 no convergence, 2 completion failed).
+void jacobi_grid(corutv_handle* h, const double* X, int nv, int len, int64_t ldx, double* sig_out, int* status,
+                 double* ut, int64_t ldut, double* vt, int64_t ldvt) {
+  const int n = nv + (nv > 1 && (nv & 1));
+  const int64_t ldw = round_up(len, 2), ldv = round_up(n, 2);
+  constexpr int kMaxSweeps = 100;  // dense.py:36
+  Arena ar(h);
+  double *W, *V = nullptr, *nrm, *sig;
+  int *order, *st;
+  unsigned long long* offs;
+  ar.add(&W, (size_t)n * ldw);
+  if (vt) ar.add(&V, (size_t)n * ldv);
+  ar.add(&nrm, (size_t)n);
+  ar.add(&sig, (size_t)n);
+  ar.add(&order, (size_t)n);
+  ar.add(&st, 2);
+  ar.add(&offs, kMaxSweeps);
+  ar.commit();
+  copy2d(h, X, nv, len, ldx, W, ldw);
+  if (n > nv) CK(cudaMemsetAsync(W + (int64_t)nv * ldw, 0, sizeof(double) * ldw, h->stream));
+  CK(cudaMemsetAsync(offs, 0, sizeof(unsigned long long) * kMaxSweeps, h->stream));
+  static int per_sm = [] {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, jg::jacobi_grid_kernel, jg::THREADS, 0) != cudaSuccess) {
+      cudaGetLastError();
+      b = 1;
+    }
+    return std::max(b, 1);
+  }();
+  const int warps_per_block = jg::THREADS / 32;
+  const int blocks = (int)std::max<int64_t>(
+      1, std::min<int64_t>((int64_t)per_sm * h->num_sms, (n / 2 + warps_per_block - 1) / warps_per_block));
+  double tol = 1e-14;  // dense.py:34
+  int max_sweeps = kMaxSweeps, nv_ = nv, n_ = n, len_ = len;
+  int64_t ldw_ = ldw, ldv_ = ldv;
+  void* args[] = {&W, &ldw_, &V, &ldv_, &nv_, &n_, &len_, &tol, &max_sweeps, &nrm, &offs, &sig, &order, &sig_out,
+                  &ut, &ldut, &vt, &ldvt, &st};
+  CK(cudaLaunchCooperativeKernel((const void*)jg::jacobi_grid_kernel, dim3(blocks), dim3(jg::THREADS), args, 0,
+                                 h->stream));
+  ++h->launches;
+  if (status) CK(cudaMemcpyAsync(status, st, sizeof(int), cudaMemcpyDeviceToDevice, h->stream));
+}
+
 // one-sided Jacobi: singular values of the matrix whose columns are the nv
 // rows of X (len each); optional pinv.  gwork: (n+1)*(len+n) doubles.
+// Cores that fit shared memory run in one CTA; larger ones (without pinv)
+// on the cooperative grid.
 void jacobi(corutv_handle* h, const double* X, int nv, int len, int64_t ldx, double* sig, double* pinv,
             int64_t ldp, double* gwork, int* status, double* ut = nullptr, int64_t ldut = 0,
             double* vt = nullptr, int64_t ldvt = 0) {
@@ -716,6 +764,11 @@ void jacobi(corutv_handle* h, const double* X, int nv, int len, int64_t ldx, dou
   const size_t stat = (small::LMAX * 2) * 8 + 8 * 1024;
   const bool smem = bytes + stat <= (size_t)optin;
   const int jt = (int)std::min<int64_t>(1024, std::max<int64_t>(64, 32 * (int64_t)((n + 1) / 2)));
+  if (!smem && !pinv) {
+    jacobi_grid(h, X, nv, len, ldx, sig, status, ut, ldut, vt, ldvt);
+    return;
+  }
+  if (nv > small::LMAX) fail(h, CORUTV_ERR_ARG, "pseudoinverse core above the supported maximum 640");
   if (smem) {
     set_smem(h, small::jacobi_kernel<true>, bytes);
     small::jacobi_kernel<true><<<1, jt, bytes, h->stream>>>(X, nv, len, ldx, 1e-14, 100, sig, pinv, ldp, ut, ldut,
@@ -1699,32 +1752,72 @@ int corutv_decompose_host(corutv_handle* hh, const double* a_host, int64_t m, in
   ABI_END
 }
 
-int corutv_jacobi_svd(corutv_handle* hh, const double* a, int64_t m, int64_t n, int64_t lda, double* u,
-                      double* sigma, double* v) {
-  ABI_BEGIN(hh)
-  if (!a || !u || !sigma || !v) fail(h, CORUTV_ERR_ARG, "null pointer argument");
-  if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
+// Economy SVD by one-sided Jacobi (dense.py:313-376), optionally warm
+// started from the tall orientation's right factor v_init (k x k, ld ldvi):
+// X = A_tall v_init is formed by one DMMA GEMM straight into the row-per-
+// column layout the sweeps use, and the final right factor is v_init times
+// the sorted rotations (second GEMM).  m >= n sweeps A's columns directly
+// (the reference QR-preconditions first; same decomposition to rounding).
+// u: m x k, v: n x k (ld k).  Returns the sweep-count-free status on host.
+void svd_warm(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, const double* v_init,
+              int64_t ldvi, double* u, double* sigma, double* v) {
   const int64_t k = std::min(m, n), len = std::max(m, n);
-  if (k > small::LMAX) fail(h, CORUTV_ERR_ARG, "jacobi_svd: min(m, n) above the supported maximum 640");
-  const int64_t ldl = round_up(len, 2), ldk = round_up(k, 2);
+  const bool tall = m >= n;
+  const int64_t ldl = round_up(len, 16), ldk = round_up(k, 16);
+  const bool a_ok = ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && (lda % 2 == 0);
   Arena ar(h);
-  double *X, *UT, *VT, *gw;
+  double *X, *UT, *VT, *gw, *VI = nullptr, *VIt = nullptr, *VF = nullptr, *ap = nullptr, *ws = nullptr;
   int* st;
   ar.add(&X, (size_t)k * ldl);
   ar.add(&UT, (size_t)k * ldl);
   ar.add(&VT, (size_t)k * ldk);
   ar.add(&gw, (size_t)(k + 2) * (len + k + 2) + 16);
   ar.add(&st, 4);
+  if (v_init) {
+    ar.add(&VI, (size_t)k * ldk);
+    ar.add(&VIt, (size_t)k * ldk);
+    ar.add(&VF, (size_t)k * ldk);
+    if (!a_ok) ar.add(&ap, (size_t)m * round_up(n, 16));
+    ar.add(&ws, std::max(gemm_ws_elems(h, k, len, k), gemm_ws_elems(h, k, k, k)) + 16);
+  }
   ar.commit();
-  // rotate the columns of the tall orientation (dense.py:371-376)
-  if (m >= n) transpose(h, a, m, n, lda, X, ldl);
-  else copy2d(h, a, m, n, lda, X, ldl);
-  jacobi(h, X, (int)k, (int)len, ldl, sigma, nullptr, 0, gw, st, UT, ldl, VT, ldk);
-  if (m >= n) {
-    transpose(h, UT, k, m, ldl, u, k);   // u = UT'  (m x k)
-    transpose(h, VT, k, n, ldk, v, k);   // v = VT'  (n x n)
+  if (!v_init) {
+    // rotate the columns of the tall orientation (dense.py:371-376)
+    if (tall) transpose(h, a, m, n, lda, X, ldl);
+    else copy2d(h, a, m, n, lda, X, ldl);
   } else {
-    transpose(h, VT, k, m, ldk, u, k);   // wide: factors of A' swapped
+    const double* A = a;
+    int64_t la = lda;
+    if (!a_ok) {
+      la = round_up(n, 16);
+      copy2d(h, a, m, n, lda, ap, la);
+      A = ap;
+    }
+    copy2d(h, v_init, k, k, ldvi, VI, ldk);
+    if (tall) {
+      // X (row c = column c of A v_init) = v_init' A'
+      transpose(h, VI, k, k, ldk, VIt, ldk);
+      run_gemm(h, false, k, m, k, VIt, ldk, A, la, X, ldl, nullptr, 0, ws);
+    } else {
+      // wide: the tall orientation is A', X = v_init' A
+      run_gemm(h, true, k, n, k, VI, ldk, A, la, X, ldl, nullptr, 0, ws);
+    }
+  }
+  jacobi(h, X, (int)k, (int)len, ldl, sigma, nullptr, 0, gw, st, UT, ldl, VT, ldk);
+  // right factor of the tall orientation: rotations (rows of VT), times v_init
+  const double* R = VT;
+  if (v_init) {
+    run_gemm(h, false, k, k, k, VI, ldk, VT, ldk, VF, ldk, nullptr, 0, ws);  // v_init vrot[:, order]
+    R = VF;
+  }
+  if (tall) {
+    transpose(h, UT, k, m, ldl, u, k);  // u = UT'  (m x k)
+    if (v_init) copy2d(h, R, k, k, ldk, v, k);
+    else transpose(h, R, k, n, ldk, v, k);
+  } else {
+    // wide: factors of A' swapped
+    if (v_init) copy2d(h, R, k, k, ldk, u, k);
+    else transpose(h, R, k, m, ldk, u, k);
     transpose(h, UT, k, n, ldl, v, k);
   }
   CK(cudaMemcpyAsync(h->pinned, st, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
@@ -1733,6 +1826,58 @@ int corutv_jacobi_svd(corutv_handle* hh, const double* a, int64_t m, int64_t n, 
   std::memcpy(&s0, h->pinned, sizeof(int));
   if (s0 == 1) fail(h, CORUTV_ERR_CONVERGENCE, "one-sided Jacobi did not converge in 100 sweeps");
   if (s0 == 2) fail(h, CORUTV_ERR_CONVERGENCE, "orthonormal completion ran out of candidates");
+}
+
+constexpr int64_t kSvdMax = 16384;  // X, U', V' and the sweep copies of one core
+
+int corutv_jacobi_svd(corutv_handle* hh, const double* a, int64_t m, int64_t n, int64_t lda, double* u,
+                      double* sigma, double* v) {
+  ABI_BEGIN(hh)
+  if (!a || !u || !sigma || !v) fail(h, CORUTV_ERR_ARG, "null pointer argument");
+  if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
+  if (std::min(m, n) > kSvdMax) fail(h, CORUTV_ERR_ARG, "jacobi_svd: min(m, n) above the supported maximum 16384");
+  svd_warm(h, a, m, n, lda, nullptr, 0, u, sigma, v);
+  ABI_END
+}
+
+int corutv_jacobi_svd_warm(corutv_handle* hh, const double* a, int64_t m, int64_t n, int64_t lda,
+                           const double* v_init, int64_t ldvi, double* u, double* sigma, double* v) {
+  ABI_BEGIN(hh)
+  if (!a || !u || !sigma || !v) fail(h, CORUTV_ERR_ARG, "null pointer argument");
+  if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
+  if (std::min(m, n) > kSvdMax) fail(h, CORUTV_ERR_ARG, "jacobi_svd: min(m, n) above the supported maximum 16384");
+  if (v_init && ldvi < std::min(m, n)) fail(h, CORUTV_ERR_ARG, "leading dimension of v_init < min(m, n)");
+  svd_warm(h, a, m, n, lda, v_init, ldvi, u, sigma, v);
+  ABI_END
+}
+
+int corutv_svt(corutv_handle* hh, const double* b, int64_t m, int64_t n, int64_t ldb, double delta, int cap,
+               const double* v_init, int64_t ldvi, double* u, double* kept, double* v, double* t, int* r_host) {
+  ABI_BEGIN(hh)
+  if (!b || !u || !kept || !v || !t) fail(h, CORUTV_ERR_ARG, "null pointer argument");
+  if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "b must have positive dimensions");
+  if (!(delta >= 0.0)) fail(h, CORUTV_ERR_ARG, "delta must be >= 0");
+  const int64_t k = std::min(m, n);
+  if (k > kSvdMax) fail(h, CORUTV_ERR_ARG, "svt: min(m, n) above the supported maximum 16384");
+  if (v_init && ldvi < k) fail(h, CORUTV_ERR_ARG, "leading dimension of v_init < min(m, n)");
+  Arena ar(h);
+  double* sig;
+  int* cnt;
+  ar.add(&sig, (size_t)k);
+  ar.add(&cnt, 1);
+  ar.commit();
+  svd_warm(h, b, m, n, ldb, v_init, ldvi, u, sig, v);
+  CK(cudaMemsetAsync(cnt, 0, sizeof(int), h->stream));
+  int nb, tb;
+  launch_grid_1d(k * k, &nb, &tb);
+  aux::svt_kept_kernel<<<nb, tb, 0, h->stream>>>(sig, (int)k, delta, kept, t, k, cnt);
+  CK_LAUNCH();
+  CK(cudaMemcpyAsync(h->pinned, cnt, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  sync(h);
+  int r = 0;
+  std::memcpy(&r, h->pinned, sizeof(int));
+  if (cap >= 0) r = std::min(r, cap);  // rpca.py:152-153
+  if (r_host) *r_host = r;
   ABI_END
 }
 

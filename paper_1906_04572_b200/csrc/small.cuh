@@ -365,6 +365,47 @@ __global__ void __launch_bounds__(1024, 1)
   }
 }
 
+// Left-factor completion for zero singular values (dense.py:285-310), one
+// warp: row j of ut (sorted order, sig_sorted[j] == 0) is replaced by the
+// first unit-vector candidate e_cand that keeps norm > 0.1 after two
+// Gram-Schmidt passes against the kept rows (index order) and the earlier
+// fills.  Returns true when the candidates run out.
+__device__ bool complete_left(double* ut_out, int64_t ldut, const double* sig_sorted, int nv, int len,
+                              int lane) {
+  int cand = 0;
+  for (int j = 0; j < nv; ++j) {
+    if (sig_sorted[j] > 0.0) continue;
+    for (;;) {
+      if (cand >= len) return true;
+      for (int i = lane; i < len; i += 32) ut_out[j * ldut + i] = (i == cand) ? 1.0 : 0.0;
+      ++cand;
+      __syncwarp();
+      for (int pass = 0; pass < 2; ++pass) {
+        // basis: kept vectors (sig > 0) in index order, then earlier fills
+        for (int b = 0; b < 2 * nv; ++b) {
+          const int kb = b < nv ? b : b - nv;
+          const bool kept = sig_sorted[kb] > 0.0;
+          if (b < nv ? !kept : (kept || kb >= j)) continue;
+          double d = 0.0;
+          for (int i = lane; i < len; i += 32) d += ut_out[kb * ldut + i] * ut_out[j * ldut + i];
+          d = warp_sum(d);
+          for (int i = lane; i < len; i += 32) ut_out[j * ldut + i] -= d * ut_out[kb * ldut + i];
+          __syncwarp();
+        }
+      }
+      double nw = 0.0;
+      for (int i = lane; i < len; i += 32) nw += ut_out[j * ldut + i] * ut_out[j * ldut + i];
+      nw = sqrt(warp_sum(nw));
+      if (nw > 0.1) {
+        for (int i = lane; i < len; i += 32) ut_out[j * ldut + i] /= nw;
+        __syncwarp();
+        break;
+      }
+    }
+  }
+  return false;
+}
+
 // ---------------------------------------------------------------- Jacobi
 // One-sided Jacobi on the nv rows (length len, ld ldx) of X: orthogonalises
 // them by plane rotations in the round-robin order of dense.py:200-210,
@@ -507,45 +548,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     __syncthreads();
     // zero singular values: complete the left factor (dense.py:285-310)
-    // with unit-vector candidates, Gram-Schmidt'ed twice against the kept
-    // vectors in index order, accepted above norm 0.1
-    if (ut_out && warp == 0) {
-      int cand = 0;
-      for (int j = 0; j < nv; ++j) {
-        if (sig[order[j]] > 0.0) continue;
-        for (;;) {
-          if (cand >= len) {
-            st = 2;
-            break;
-          }
-          for (int i = lane; i < len; i += 32) ut_out[j * ldut + i] = (i == cand) ? 1.0 : 0.0;
-          ++cand;
-          __syncwarp();
-          for (int pass = 0; pass < 2; ++pass) {
-            // basis: kept vectors (sig > 0) in index order, then earlier fills
-            for (int b = 0; b < 2 * nv; ++b) {
-              const int kb = b < nv ? b : b - nv;
-              const bool kept = sig[order[kb]] > 0.0;
-              if (b < nv ? !kept : (kept || kb >= j)) continue;
-              double d = 0.0;
-              for (int i = lane; i < len; i += 32) d += ut_out[kb * ldut + i] * ut_out[j * ldut + i];
-              d = warp_sum(d);
-              for (int i = lane; i < len; i += 32) ut_out[j * ldut + i] -= d * ut_out[kb * ldut + i];
-              __syncwarp();
-            }
-          }
-          double nw = 0.0;
-          for (int i = lane; i < len; i += 32) nw += ut_out[j * ldut + i] * ut_out[j * ldut + i];
-          nw = sqrt(warp_sum(nw));
-          if (nw > 0.1) {
-            for (int i = lane; i < len; i += 32) ut_out[j * ldut + i] /= nw;
-            __syncwarp();
-            break;
-          }
-        }
-        if (st == 2) break;
-      }
-    }
+    if (ut_out && warp == 0 && complete_left(ut_out, ldut, sig_out, nv, len, lane)) st = 2;
   }
   if (threadIdx.x == 0 && status) *status = st;
 }

@@ -4,6 +4,8 @@
 * :func:`spectral_norm` — dense.py:405-442 (mu0 of the ALM solver)
 * :func:`singular_values` — dense.py:379-387 (rank readout of L)
 * :func:`frobenius_norm` — dense.py:94-96
+* :func:`jacobi_svd` — dense.py:313-376 (sor_svd / tsr_svd cores, the
+  InexactALM baseline's warm-started SVT)
 """
 
 from __future__ import annotations
@@ -16,7 +18,10 @@ from . import _device as dev
 from . import _lib
 
 __all__ = ["spectral_norm", "singular_values", "frobenius_norm", "spectral_norm_iters", "SvdFactors",
-           "jacobi_svd"]
+           "jacobi_svd", "JACOBI_TOL", "JACOBI_MAX_SWEEPS"]
+
+JACOBI_TOL = 1e-14        # dense.py:34
+JACOBI_MAX_SWEEPS = 100   # dense.py:36
 
 
 @dataclass
@@ -77,17 +82,38 @@ def frobenius_norm(a) -> float:
     return math.sqrt(out.value)
 
 
-def jacobi_svd(a) -> SvdFactors:
-    """dense.py:357-376 (no warm start) on the device: economy SVD of a
-    matrix with min(m, n) <= 640 (corutv_jacobi_svd)."""
+def _check_v_init(v_init, k: int):
+    """dense.py:316-318: v_init must be the k x k right factor of the tall
+    orientation."""
+    V, _ = dev.to_device(v_init, "v_init")
+    dev.raise_if_nonfinite(V, "v_init")
+    if tuple(V.shape) != (k, k):
+        raise ValueError(f"v_init must be {k}x{k}, got {tuple(V.shape)}")
+    return V
+
+
+def jacobi_svd(a, tol: float = JACOBI_TOL, max_sweeps: int = JACOBI_MAX_SWEEPS,
+               v_init=None) -> SvdFactors:
+    """dense.py:357-376 on the device: economy SVD by one-sided Jacobi
+    (min(m, n) <= 16384; one CTA when the core fits shared memory, else a
+    cooperative grid, jacobi_grid.cuh).  ``v_init`` warm-starts the sweeps
+    from the tall orientation's right factor (corutv_jacobi_svd_warm).
+    tol / max_sweeps are fixed at the reference defaults 1e-14 / 100."""
+    if tol != JACOBI_TOL or max_sweeps != JACOBI_MAX_SWEEPS:
+        raise ValueError("jacobi_svd runs with the reference defaults tol=1e-14, max_sweeps=100")
     torch = dev.torch_mod()
     A, was_host = dev.to_device(a, "a")
     dev.raise_if_nonfinite(A, "a")
     m, n = A.shape
     k = min(m, n)
+    V0 = _check_v_init(v_init, k).contiguous() if v_init is not None else None
     u = torch.empty((m, k), dtype=torch.float64, device=A.device)
     s = torch.empty((k,), dtype=torch.float64, device=A.device)
     v = torch.empty((n, k), dtype=torch.float64, device=A.device)
     h = _lib.handle(A.device.index)
-    h.call("corutv_jacobi_svd", dev.ptr(A), m, n, A.stride(0), dev.ptr(u), dev.ptr(s), dev.ptr(v))
+    if V0 is None:
+        h.call("corutv_jacobi_svd", dev.ptr(A), m, n, A.stride(0), dev.ptr(u), dev.ptr(s), dev.ptr(v))
+    else:
+        h.call("corutv_jacobi_svd_warm", dev.ptr(A), m, n, A.stride(0), dev.ptr(V0), V0.stride(0),
+               dev.ptr(u), dev.ptr(s), dev.ptr(v))
     return SvdFactors(u=dev.to_output(u, was_host), sigma=dev.to_output(s, was_host), v=dev.to_output(v, was_host))

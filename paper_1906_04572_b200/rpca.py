@@ -33,6 +33,8 @@ __all__ = [
     "shrink",
     "corutv_threshold",
     "alm_corutv",
+    "inexact_alm",
+    "svt",
     "write_telemetry_csv",
 ]
 
@@ -137,10 +139,50 @@ def corutv_threshold(b, delta: float, cfg: SketchConfig):
     return dev.to_output(_lowrank_device(f.u, f.t, f.v, r), was_host), r
 
 
-def alm_corutv(m, cfg: AlmConfig) -> RpcaSolution:
-    """rpca.py:237-255 (+ _alm_loop rpca.py:175-234) on the device."""
-    if cfg.ell is None:
-        raise ValueError("alm_corutv requires cfg.ell (sketch sample size)")
+def _svt_device(B, delta: float, cap, v_init):
+    """_svt_warm rpca.py:146-158 on the device (corutv_svt): returns
+    (u, t, v, k, r, kept) with u[:, :r] (t[:r, :] v') the thresholded matrix
+    and v the warm start of the next call."""
+    torch = dev.torch_mod()
+    m_, n_ = B.shape
+    k = min(m_, n_)
+    V0 = None
+    if v_init is not None:
+        if tuple(v_init.shape) != (k, k):
+            raise ValueError(f"v_init must be {k}x{k}, got {tuple(v_init.shape)}")
+        V0 = v_init
+    u = torch.empty((m_, k), dtype=torch.float64, device=B.device)
+    v = torch.empty((n_, k), dtype=torch.float64, device=B.device)
+    t = torch.empty((k, k), dtype=torch.float64, device=B.device)
+    kept = torch.empty((k,), dtype=torch.float64, device=B.device)
+    r = ctypes.c_int(0)
+    h = _lib.handle(B.device.index)
+    h.call("corutv_svt", dev.ptr(B), m_, n_, B.stride(0), delta, -1 if cap is None else int(cap),
+           dev.ptr(V0) if V0 is not None else None, V0.stride(0) if V0 is not None else 0,
+           dev.ptr(u), dev.ptr(kept), dev.ptr(v), dev.ptr(t), ctypes.byref(r))
+    return u, t, v, k, int(r.value), kept
+
+
+def svt(b, delta: float):
+    """rpca.py:135-143: singular value thresholding by the full Jacobi SVD
+    (device, min(m, n) <= 16384); returns ``(matrix, r)``."""
+    if delta < 0:
+        raise ValueError("delta must be >= 0")
+    torch = dev.torch_mod()
+    B, was_host = dev.to_device(b, "b")
+    dev.raise_if_nonfinite(B, "b")
+    u, t, v, k, r, _ = _svt_device(B, float(delta), None, None)
+    if r == 0:
+        return dev.to_output(torch.zeros_like(B), was_host), 0
+    return dev.to_output(_lowrank_device(u, t, v, r), was_host), r
+
+
+def _alm_loop(m, cfg: AlmConfig, step, cap0) -> RpcaSolution:
+    """rpca.py:175-234 on the device.  ``step(g, delta, cap, j, state)``
+    returns (u, t, v, ell, rank, sigma_thunk, state): the thresholded iterate
+    is u[:, :rank] (t[:rank, :] v'), kept implicit and fused into the ALM
+    update (corutv_alm_update); sigma_thunk() gives the spectrum behind
+    rank_of_l once the loop stops."""
     torch = dev.torch_mod()
     M, was_host = dev.to_device(m, "m")
     if M.stride(0) != M.shape[1]:
@@ -162,7 +204,7 @@ def alm_corutv(m, cfg: AlmConfig) -> RpcaSolution:
     mu_bar = cfg.mu_bar if cfg.mu_bar is not None else 1e7 * mu
     limit = min(h_, w_)
     grow = max(1, round(0.05 * limit))
-    cap = max(1, min(cfg.ell, limit))
+    cap = max(1, min(cap0 if cap0 is not None else limit, limit))
     y = torch.zeros_like(M)
     s = torch.zeros_like(M)
     g = torch.empty_like(M)
@@ -170,16 +212,14 @@ def alm_corutv(m, cfg: AlmConfig) -> RpcaSolution:
     residuals, ranks, nnzs, mus, caps = [], [], [], [], []
     zeta2 = ctypes.c_double(0.0)
     nnz = ctypes.c_int64(0)
+    state = None
     for j in range(cfg.max_iter):
-        scfg = SketchConfig(ell=cap, q_power=cfg.q_power, seed=(cfg.seed + j) % 2 ** 64)
-        # Omega = gaussian_matrix(w, cap, seed + j) drawn on the device; the
-        # rank count r = #(|diag T| > 1/mu) comes back with the factors
-        f, rank = corutv_truncated(src, scfg, 1.0 / mu)
+        u, t, v, ell, rank, sigma_of, state = step(src, 1.0 / mu, cap, j, state)
         caps.append(cap)
         cap = _next_cap(cap, rank, limit, grow)
         mu_next = min(cfg.rho * mu, mu_bar)
         handle.call("corutv_alm_update", dev.ptr(M), dev.ptr(s), dev.ptr(y), dev.ptr(g), h_, w_,
-                    dev.ptr(f.u), dev.ptr(f.t), dev.ptr(f.v), f.ell, rank, mu, lam / mu, mu_next,
+                    dev.ptr(u), dev.ptr(t), dev.ptr(v), ell, rank, mu, lam / mu, mu_next,
                     ctypes.byref(zeta2), ctypes.byref(nnz))
         src = g
         zeta = float(np.sqrt(zeta2.value)) / norm_m
@@ -189,9 +229,8 @@ def alm_corutv(m, cfg: AlmConfig) -> RpcaSolution:
         mus.append(mu)
         if zeta < cfg.tol:
             if rank > 0:
-                l_mat = _lowrank_device(f.u, f.t, f.v, rank)
-                sig = singular_values(f.t[:rank, :])
-                sig = sig.cpu().numpy() if dev.is_device_tensor(sig) else sig
+                l_mat = _lowrank_device(u, t, v, rank)
+                sig = sigma_of()
             else:
                 l_mat = torch.zeros_like(M)
                 sig = np.zeros(0)
@@ -208,6 +247,41 @@ def alm_corutv(m, cfg: AlmConfig) -> RpcaSolution:
         residual=residuals[-1],
         history=residuals,
     )
+
+
+def alm_corutv(m, cfg: AlmConfig) -> RpcaSolution:
+    """rpca.py:237-255 (+ _alm_loop rpca.py:175-234) on the device."""
+    if cfg.ell is None:
+        raise ValueError("alm_corutv requires cfg.ell (sketch sample size)")
+
+    def step(g, delta, cap, j, state):
+        scfg = SketchConfig(ell=cap, q_power=cfg.q_power, seed=(cfg.seed + j) % 2 ** 64)
+        # Omega = gaussian_matrix(w, cap, seed + j) drawn on the device; the
+        # rank count r = #(|diag T| > 1/mu) comes back with the factors
+        f, rank = corutv_truncated(g, scfg, delta)
+
+        def sigma_of():
+            sig = singular_values(f.t[:rank, :])
+            return sig.cpu().numpy() if dev.is_device_tensor(sig) else sig
+
+        return f.u, f.t, f.v, f.ell, rank, sigma_of, None
+
+    return _alm_loop(m, cfg, step, cap0=cfg.ell)
+
+
+def inexact_alm(m, cfg: AlmConfig) -> RpcaSolution:
+    """rpca.py:258-273: the InexactALM baseline on the device.  Each
+    iteration thresholds G_j by a full one-sided Jacobi SVD warm-started
+    from the previous right factor (corutv_svt), the kept rank capped by the
+    same prediction schedule; the thresholded iterate stays implicit
+    (u, diag(kept), v) and feeds the same fused ALM update."""
+
+    def step(g, delta, cap, j, state):
+        u, t, v, k, r, kept = _svt_device(g, delta, cap, state)
+        return u, t, v, k, r, (lambda: kept[:r].cpu().numpy()), v
+
+    # cap0 = cfg.ell, else min(m.shape) (rpca.py:272)
+    return _alm_loop(m, cfg, step, cap0=cfg.ell)
 
 
 def write_telemetry_csv(solution: RpcaSolution, path) -> None:

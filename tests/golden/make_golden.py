@@ -145,6 +145,58 @@ put("alm_n400", "rpca.alm_corutv(gen_rpca_instance(n=400, seed=0), AlmConfig(ell
     s_support=np.flatnonzero(np.abs(sol.s) > 1e-12).astype(np.int32),
     l_sample=sol.l[::37, ::41], s_sample=sol.s[::37, ::41])
 
+# ---- warm-started Jacobi SVD (dense.py:313-376, v_init) ------------------
+g = np.random.Generator(np.random.PCG64(31))
+a = g.standard_normal((24, 24))
+v0 = rdense.jacobi_svd(a + 1e-3 * g.standard_normal((24, 24))).v
+f = rdense.jacobi_svd(a, v_init=v0)
+put("svdwarm_sq", "dense.jacobi_svd(a, v_init=jacobi_svd(a + 1e-3 E).v), 24x24", a=a, v_init=v0, u=f.u,
+    sigma=f.sigma, v=f.v)
+a = g.standard_normal((30, 17))
+v0 = rdense.jacobi_svd(a + 1e-3 * g.standard_normal((30, 17))).v
+f = rdense.jacobi_svd(a, v_init=v0)
+put("svdwarm_tall", "dense.jacobi_svd(a, v_init=...), 30x17 (odd width: pad column)", a=a, v_init=v0, u=f.u,
+    sigma=f.sigma, v=f.v)
+a = g.standard_normal((13, 29))
+v0 = rdense.jacobi_svd(a.T + 1e-3 * g.standard_normal((29, 13))).v
+f = rdense.jacobi_svd(a, v_init=v0)
+put("svdwarm_wide", "dense.jacobi_svd(a, v_init=...), 13x29 (v_init: right factor of a')", a=a, v_init=v0,
+    u=f.u, sigma=f.sigma, v=f.v)
+
+# ---- svt (rpca.py:135-158) -------------------------------------------------
+g = np.random.Generator(np.random.PCG64(41))
+for name, b, delta in (("svt_diag", np.diag([3.0, 1.0]), 2.0),          # test_rpca.py:52-55
+                       ("svt_zero", g.standard_normal((6, 5)), 0.0),    # test_rpca.py:58-62
+                       ("svt_nuc", g.standard_normal((20, 20)), 1.5),   # test_rpca.py:65-72
+                       ("svt_wide", g.standard_normal((9, 16)), 0.8),
+                       ("svt_rank", rank_k(42, 40, 40, 4) + 1e-3 * g.standard_normal((40, 40)), 0.5)):
+    mat, r = rrpca.svt(b, delta)
+    put(name, f"rpca.svt(b, {delta})", b=b, delta=delta, mat=mat, r=r)
+
+# ---- InexactALM baseline (rpca.py:258-273) ---------------------------------
+for n, seed in ((60, 7), (100, 3)):
+    k, s, m, l0, s0 = instance(n, seed)
+    sol = rrpca.inexact_alm(m, rrpca.AlmConfig(ell=2 * k))
+    put(f"ialm_n{n}", f"rpca.inexact_alm(gen_rpca_instance(n={n}, seed={seed}), AlmConfig(ell={2*k}))",
+        m=m, l=sol.l, s=sol.s, iterations=sol.iterations, residuals=sol.residuals,
+        rank_of_l=sol.rank_of_l, nnz_of_s=sol.nnz_of_s, rank_history=sol.rank_history,
+        nnz_history=sol.nnz_history, mu_history=sol.mu_history, ell_history=sol.ell_history)
+k, s, m, l0, s0 = instance(80, 3)  # test_rpca.py:139-143: max_iter error carries the history
+try:
+    rrpca.inexact_alm(m, rrpca.AlmConfig(max_iter=2))
+except rdense.ConvergenceError as exc:
+    put("ialm_maxiter", "rpca.inexact_alm(gen_rpca_instance(n=80, seed=3), AlmConfig(max_iter=2)) -> ConvergenceError",
+        m=m, history=exc.history, residual=exc.residual)
+# desk scale n=400 (test_rpca.py:176-180): histories + support only
+k, s, m, l0, s0 = instance(400, 0)
+sol = rrpca.inexact_alm(m, rrpca.AlmConfig(ell=2 * k))
+put("ialm_n400", "rpca.inexact_alm(gen_rpca_instance(n=400, seed=0), AlmConfig(ell=40)); M regenerated by oracle.gen_rpca_instance",
+    iterations=sol.iterations, residuals=sol.residuals, rank_of_l=sol.rank_of_l, nnz_of_s=sol.nnz_of_s,
+    rank_history=sol.rank_history, nnz_history=sol.nnz_history, mu_history=sol.mu_history,
+    ell_history=sol.ell_history, m_sum=m.sum(),
+    s_support=np.flatnonzero(np.abs(sol.s) > 1e-12).astype(np.int32),
+    l_sample=sol.l[::37, ::41], s_sample=sol.s[::37, ::41])
+
 here = Path(__file__).resolve().parent
 np.savez_compressed(here / "golden.npz", **out)
 (here / "golden.json").write_text(json.dumps(meta, indent=1, sort_keys=True) + "\n")

@@ -142,3 +142,52 @@ def test_svd_sketches_match_reference(golden, name):
     assert f["passes"] == int(c["passes"])
     assert np.array_equal(f["sigma"], c["sigma"])
     assert np.array_equal(f["u"], c["u"]) and np.array_equal(f["v"], c["v"])
+
+
+# ---- InexactALM baseline pieces --------------------------------
+
+@pytest.mark.parametrize("name", ["svdwarm_sq", "svdwarm_tall", "svdwarm_wide"])
+def test_warm_jacobi_svd_matches_reference(golden, name):
+    c = golden[name]
+    u, s, v = O.jacobi_svd(c["a"], c["v_init"])
+    assert np.array_equal(s, c["sigma"])
+    assert np.array_equal(u, c["u"]) and np.array_equal(v, c["v"])
+
+
+def test_warm_jacobi_rejects_wrong_v_init(golden):
+    c = golden["svdwarm_wide"]
+    with pytest.raises(ValueError, match="v_init must be 13x13"):
+        O.jacobi_svd(c["a"], np.eye(29))
+
+
+@pytest.mark.parametrize("name", ["svt_diag", "svt_zero", "svt_nuc", "svt_wide", "svt_rank"])
+def test_svt_matches_reference(golden, name):
+    c = golden[name]
+    mat, r = O.svt(c["b"], float(c["delta"]))
+    assert r == int(c["r"])
+    assert np.array_equal(mat, c["mat"])
+
+
+@pytest.mark.parametrize("n", [60, 100])
+def test_inexact_alm_matches_reference(golden, n):
+    c = golden[f"ialm_n{n}"]
+    sol = O.inexact_alm(c["m"], ell=int(c["ell_history"][0]))
+    assert sol["iterations"] == int(c["iterations"])
+    for key in ("rank_history", "nnz_history", "ell_history"):
+        assert sol[key] == [int(x) for x in c[key]]
+    assert np.array_equal(np.array(sol["residuals"]), c["residuals"])
+    assert np.array_equal(np.array(sol["mu_history"]), c["mu_history"])
+    assert sol["rank_of_l"] == int(c["rank_of_l"]) and sol["nnz_of_s"] == int(c["nnz_of_s"])
+    assert np.array_equal(sol["l"], c["l"]) and np.array_equal(sol["s"], c["s"])
+
+
+def test_inexact_alm_max_iter_history_matches_reference(golden):
+    c = golden["ialm_maxiter"]
+    with pytest.raises(O.OracleConvergenceError) as exc:
+        O.inexact_alm(c["m"], max_iter=2)
+    assert np.array_equal(np.array(exc.value.history), c["history"])
+
+
+def test_inexact_alm_zero_matrix():
+    sol = O.inexact_alm(np.zeros((30, 30)))
+    assert sol["iterations"] == 1 and not sol["l"].any() and not sol["s"].any()
