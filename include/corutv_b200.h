@@ -223,6 +223,20 @@ int corutv_alm_update(corutv_handle* h, const double* m_mat, double* s, double* 
 int corutv_lowrank(corutv_handle* h, const double* u, const double* t, const double* v,
                    int64_t rows, int64_t cols, int ell, int r, double* l_out);
 
+/* corutv_lowrank_error with only the leading r rows of T kept:
+ * |A - U[:, :r] (T[:r, :] V')|_F, the truncated-UTV error of bench.py's
+ * "utv-approx" method (bench.py:219-222).  0 <= r <= ell. */
+int corutv_lowrank_error_rank(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda,
+                              const double* u, const double* t, const double* v, int ell, int r,
+                              double* out_host);
+
+/* Column-pivoted QR of a square n x n device matrix (dense.py:152-192,
+ * Businger-Golub pivoting, first-index ties): q (n x n), r (n x n, upper),
+ * perm (n) with a[:, perm] = q r.  n <= 640.  The harness's deterministic
+ * "qrcp" method (bench.py:151-152, 208-211). */
+int corutv_qrcp(corutv_handle* h, const double* a, int64_t n, int64_t lda, double* q, double* r,
+                int64_t* perm);
+
 /* |A|_2 by block power iteration — dense.py:405-442 (b = min(24, n),
  * disjoint-support start, stop when |est - prev| <= 0.02 tol est).
  * Matrices with min(m, n) <= 64 use the one-sided Jacobi path

@@ -52,6 +52,8 @@ SIGNATURES = {
     "corutv_download": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _I64]),
     "corutv_jacobi_svd": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _VP, _VP]),
     "corutv_jacobi_svd_warm": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _I64, _VP, _VP, _VP]),
+    "corutv_lowrank_error_rank": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _VP, _VP, _I32, _I32, c_double_p]),
+    "corutv_qrcp": (_I32, [_VP, _VP, _I64, _I64, _VP, _VP, _VP]),
     "corutv_svt": (_I32, [_VP, _VP, _I64, _I64, _I64, _D, _I32, _VP, _I64, _VP, _VP, _VP, _VP,
                           ctypes.POINTER(_I32)]),
     "corutv_sor_svd": (_I32, [_VP, _VP, _I64, _I64, _I64, _I32, _I32, _I32, _VP, _VP, _VP, _VP, _VP,

@@ -2116,6 +2116,41 @@ int corutv_lowrank_error(corutv_handle* hh, const double* a, int64_t m, int64_t 
   ABI_END
 }
 
+int corutv_lowrank_error_rank(corutv_handle* hh, const double* a, int64_t m, int64_t n, int64_t lda,
+                              const double* u, const double* t, const double* v, int ell, int r,
+                              double* out_host) {
+  ABI_BEGIN(hh)
+  if (r < 0 || r > ell) fail(h, CORUTV_ERR_ARG, "rank outside [0, ell]");
+  gemm::LrParams p{};
+  p.ld = lda;
+  p.m_mat = a;
+  double o[2] = {0, 0};
+  lowrank_op(h, gemm::LR_RESID, u, t, v, m, n, ell, r, p, o);
+  if (out_host) *out_host = std::sqrt(o[0]);
+  ABI_END
+}
+
+int corutv_qrcp(corutv_handle* hh, const double* a, int64_t n, int64_t lda, double* q, double* r,
+                int64_t* perm) {
+  ABI_BEGIN(hh)
+  if (!a || !q || !r || !perm) fail(h, CORUTV_ERR_ARG, "null pointer argument");
+  if (n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
+  if (n > small::LMAX) fail(h, CORUTV_ERR_ARG, "qrcp: n above the supported maximum 640");
+  if (lda < n) fail(h, CORUTV_ERR_ARG, "lda < n");
+  const int l = (int)n;
+  const int64_t ldp = round_up(l, 16);
+  Arena ar(h);
+  double *qtT, *gwork;
+  int* perm32;
+  ar.add(&qtT, (size_t)l * ldp);
+  ar.add(&gwork, (size_t)(l + 2) * (2 * l + 4) + 2 * (size_t)l * l + 16);
+  ar.add(&perm32, (size_t)ldp);
+  ar.commit();
+  qrcp(h, a, l, lda, r, l, qtT, ldp, reinterpret_cast<long long*>(perm), perm32, gwork);
+  transpose(h, qtT, l, l, ldp, q, l);  // Q = qtT'
+  ABI_END
+}
+
 int corutv_spectral_norm(corutv_handle* hh, const double* a, int64_t m, int64_t n, int64_t lda, double tol,
                          int max_iter, double* out_host, int* iters_host) {
   ABI_BEGIN(hh)

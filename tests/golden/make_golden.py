@@ -197,6 +197,29 @@ put("ialm_n400", "rpca.inexact_alm(gen_rpca_instance(n=400, seed=0), AlmConfig(e
     s_support=np.flatnonzero(np.abs(sol.s) > 1e-12).astype(np.int32),
     l_sample=sol.l[::37, ::41], s_sample=sol.s[::37, ::41])
 
+# ---- experiment harness (bench.py:165-306) -------------------
+from corutv import bench as rbench  # noqa: E402
+
+for exp in ("sv-compare", "lowrank-error"):
+    cfg = rbench.ExperimentConfig(experiment=exp, n=80, k=6, trials=3, q_power=1,
+                                  methods=("svd", "qrcp", "utv-approx", "corutv", "tsr-svd", "sor-svd"))
+    rows = (rbench.run_sv_compare if exp == "sv-compare" else rbench.run_lowrank_error)(cfg)
+    cols = list(zip(*rows))
+    put(f"harness_{exp.replace('-', '_')}",
+        f"bench.run_{exp.replace('-', '_')}(ExperimentConfig({exp!r}, n=80, k=6, trials=3, q_power=1, all methods))",
+        c0=np.array(cols[0]), method=np.array(cols[1]), c2=np.array(cols[2]), c3=np.array(cols[3]),
+        c4=np.array(cols[4]))
+a_h, _ = rsynth.gen_noisy_lowrank(rsynth.NoisyLowRankSpec(n=80, k=6, seed=0, noise_coeff=0.1))
+a_0, _ = rsynth.gen_noisy_lowrank(rsynth.NoisyLowRankSpec(n=50, k=4, seed=3, noise_coeff=0.0))
+put("synth_noisy", "synth.gen_noisy_lowrank(NoisyLowRankSpec(n=80, k=6, seed=0)) and (n=50, k=4, seed=3, noise 0)",
+    a=a_h, a_noiseless=a_0)
+cfg = rbench.ExperimentConfig(experiment="rpca-recovery", sizes=(60, 80))
+rows = rbench.run_rpca_recovery(cfg)
+cols = list(zip(*rows))
+put("harness_rpca_recovery", "bench.run_rpca_recovery(ExperimentConfig('rpca-recovery', sizes=(60, 80)))",
+    n=np.array(cols[0]), solver=np.array(cols[1]), rank_l=np.array(cols[2]), nnz_s=np.array(cols[3]),
+    iters=np.array(cols[4]), zeta=np.array(cols[5]), flops=np.array(cols[6]))
+
 here = Path(__file__).resolve().parent
 np.savez_compressed(here / "golden.npz", **out)
 (here / "golden.json").write_text(json.dumps(meta, indent=1, sort_keys=True) + "\n")
