@@ -244,8 +244,10 @@ int corutv_qrcp(corutv_handle* h, const double* a, int64_t n, int64_t lda, doubl
 int corutv_spectral_norm(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda,
                          double tol, int max_iter, double* out_host, int* iters_host);
 
-/* Singular values (descending) of a small m x n matrix — dense.py:379-387
- * (one-sided Jacobi, tol 1e-14, <= 100 sweeps).  sig: min(m,n) doubles. */
+/* Singular values (descending) of an m x n matrix — dense.py:379-387
+ * (one-sided Jacobi, tol 1e-14, <= 100 sweeps; one CTA when the columns fit
+ * shared memory, else the cooperative grid), min(m, n) <= 16384.
+ * sig: min(m,n) doubles. */
 int corutv_singular_values(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda,
                            double* sig);
 

@@ -1487,13 +1487,13 @@ double sumsq(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t ld
 void singular_values(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, double* sig) {
   if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
   const int64_t k = std::min(m, n);
-  if (k > small::LMAX) fail(h, CORUTV_ERR_ARG, "singular_values: matrix too large for the small-matrix path");
+  if (k > 16384) fail(h, CORUTV_ERR_ARG, "singular_values: min(m, n) above the supported maximum 16384");
   const int64_t len = std::max(m, n);
   Arena ar(h);
   double *xt = nullptr, *gw;
   int* st;
   if (m >= n) ar.add(&xt, (size_t)n * len);
-  ar.add(&gw, (size_t)(k + 2) * (len + k + 2));
+  ar.add(&gw, 16);  // no pinv: one CTA in shared memory or the cooperative grid
   ar.add(&st, 4);
   ar.commit();
   const double* X = a;
@@ -1771,7 +1771,7 @@ void svd_warm(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t l
   ar.add(&X, (size_t)k * ldl);
   ar.add(&UT, (size_t)k * ldl);
   ar.add(&VT, (size_t)k * ldk);
-  ar.add(&gw, (size_t)(k + 2) * (len + k + 2) + 16);
+  ar.add(&gw, 16);  // no pinv: one CTA in shared memory or the cooperative grid
   ar.add(&st, 4);
   if (v_init) {
     ar.add(&VI, (size_t)k * ldk);

@@ -430,8 +430,8 @@ __global__ void __launch_bounds__(THREADS, 2)
       if (MODE != LR_STORE && row < BM && grow < t.M && c < ncols) {
         const int64_t idx = (int64_t)grow * p.ld + n0 + c;
         if (pair) {
-          mv[q] = *reinterpret_cast<const double2*>(p.m_mat + idx);
-          if (MODE == LR_ALM) yv[q] = *reinterpret_cast<const double2*>(p.y + idx);
+          mv[q] = __ldcs(reinterpret_cast<const double2*>(p.m_mat + idx));
+          if (MODE == LR_ALM) yv[q] = __ldcs(reinterpret_cast<const double2*>(p.y + idx));
         } else {
           mv[q].x = p.m_mat[idx];
           if (c + 1 < ncols) mv[q].y = p.m_mat[idx + 1];
@@ -481,9 +481,10 @@ __global__ void __launch_bounds__(THREADS, 2)
         }
       } else if (MODE == LR_ALM) {
         if (pair) {
-          *reinterpret_cast<double2*>(p.s + idx) = make_double2(sv[0], sv[1]);
-          *reinterpret_cast<double2*>(p.y + idx) = make_double2(yn[0], yn[1]);
-          *reinterpret_cast<double2*>(p.g_next + idx) = make_double2(gv[0], gv[1]);
+          // streaming (evict-first) stores: none of S, Y, G is re-read from L2
+          __stcs(reinterpret_cast<double2*>(p.s + idx), make_double2(sv[0], sv[1]));
+          __stcs(reinterpret_cast<double2*>(p.y + idx), make_double2(yn[0], yn[1]));
+          __stcs(reinterpret_cast<double2*>(p.g_next + idx), make_double2(gv[0], gv[1]));
         } else {
           p.s[idx] = sv[0]; p.y[idx] = yn[0]; p.g_next[idx] = gv[0];
           if (c + 1 < ncols) { p.s[idx + 1] = sv[1]; p.y[idx + 1] = yn[1]; p.g_next[idx + 1] = gv[1]; }

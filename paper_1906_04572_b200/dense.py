@@ -60,7 +60,8 @@ def spectral_norm(a, tol: float = 1e-10, max_iter: int = 5000) -> float:
 
 def singular_values(a):
     """Singular values, descending (dense.py:379-387), one-sided Jacobi on
-    the device.  Small matrices only (min(m, n) <= 640)."""
+    the device (one CTA, or the cooperative grid above ~116 columns;
+    min(m, n) <= 16384)."""
     torch = dev.torch_mod()
     A, was_host = dev.to_device(a, "a")
     dev.raise_if_nonfinite(A, "a")

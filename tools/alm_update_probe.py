@@ -2,10 +2,15 @@
 import ctypes
 import sys
 sys.path.insert(0, '.')
+import os
+from pathlib import Path
 import torch
 from paper_1906_04572_b200 import _lib
+if os.environ.get("CORUTV_LIB"):  # A/B a variant build of the library
+    _lib.LIB_PATH = Path(os.environ["CORUTV_LIB"]).resolve()
 torch.cuda.set_device(0)
-n, ell, r = 10000, 51, 50
+n, ell = 10000, 51
+r = int(os.environ.get("ALM_R", "50"))
 M = torch.randn(n, n, dtype=torch.float64, device='cuda')
 S = torch.zeros_like(M)
 Y = torch.zeros_like(M)
