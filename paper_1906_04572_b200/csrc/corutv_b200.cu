@@ -737,9 +737,8 @@ void jacobi_grid(corutv_handle* h, const double* X, int nv, int len, int64_t ldx
     }
     return std::max(b, 1);
   }();
-  const int warps_per_block = jg::THREADS / 32;
-  const int blocks = (int)std::max<int64_t>(
-      1, std::min<int64_t>((int64_t)per_sm * h->num_sms, (n / 2 + warps_per_block - 1) / warps_per_block));
+  // one CTA per column pair of a round
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * h->num_sms, n / 2));
   double tol = 1e-14;  // dense.py:34
   int max_sweeps = kMaxSweeps, nv_ = nv, n_ = n, len_ = len;
   int64_t ldw_ = ldw, ldv_ = ldv;

@@ -4,8 +4,10 @@
 // pairing (dense.py:200-210), cached squared column norms updated by the
 // rotation identities and clamped at 0, exact refresh after every sweep,
 // stop when max |<xa,xb>| / sqrt(|xa|^2 |xb|^2) <= tol over a sweep -- spread
-// over a cooperative grid: one warp per column pair (the n/2 pairs of a round
-// are disjoint), one grid barrier per round.  Columns live as rows of W
+// over a cooperative grid: one CTA per column pair (the n/2 pairs of a round
+// are disjoint; the CTA's warps split the rows and reduce through shared
+// memory, four 16-B loads per operand in flight per thread), one grid
+// barrier per round.  Columns live as rows of W
 // (length len, 16-B aligned, ld even) and rotations of V as rows of V, both
 // in global memory: a 1000 x 1000 problem is 16 MB, L2-resident.  No
 // __restrict__ / read-only loads here: every buffer is rewritten by other
@@ -56,6 +58,68 @@ __device__ __forceinline__ void row_rotate(double* a, double* b, int len, int la
   }
 }
 
+// Block-wide dot product of two rows (all THREADS threads; result in every
+// thread).  Four double2 loads per operand in flight per thread.
+__device__ __forceinline__ double block_row_dot(const double* a, const double* b, int len, double* red) {
+  const double2* a2 = reinterpret_cast<const double2*>(a);
+  const double2* b2 = reinterpret_cast<const double2*>(b);
+  const int h = len >> 1;
+  double s0 = 0.0, s1 = 0.0;
+  for (int i0 = threadIdx.x; i0 < h; i0 += 4 * THREADS) {
+    double2 x[4], y[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * THREADS;
+      x[u] = i < h ? a2[i] : make_double2(0.0, 0.0);
+      y[u] = i < h ? b2[i] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      s0 += x[u].x * y[u].x;
+      s1 += x[u].y * y[u].y;
+    }
+  }
+  if ((len & 1) && threadIdx.x == 0) s0 += a[len - 1] * b[len - 1];
+  const double w = warp_sum(s0 + s1);
+  __syncthreads();  // red[] is reused across calls
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = w;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int k = 0; k < THREADS / 32; ++k) t += red[k];
+  return t;
+}
+
+__device__ __forceinline__ void block_row_rotate(double* a, double* b, int len, double c, double s) {
+  double2* a2 = reinterpret_cast<double2*>(a);
+  double2* b2 = reinterpret_cast<double2*>(b);
+  const int h = len >> 1;
+  for (int i0 = threadIdx.x; i0 < h; i0 += 4 * THREADS) {
+    double2 u[4], v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = i0 + k * THREADS;
+      if (i < h) {
+        u[k] = a2[i];
+        v[k] = b2[i];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = i0 + k * THREADS;
+      if (i < h) {
+        a2[i] = make_double2(c * u[k].x - s * v[k].x, c * u[k].y - s * v[k].y);
+        b2[i] = make_double2(s * u[k].x + c * v[k].x, s * u[k].y + c * v[k].y);
+      }
+    }
+  }
+  if ((len & 1) && threadIdx.x == 0) {
+    const double u = a[len - 1], v = b[len - 1];
+    a[len - 1] = c * u - s * v;
+    b[len - 1] = s * u + c * v;
+  }
+}
+
 // W: n x len (ld ldw), rows nv..n-1 zero (odd nv padded to even n);
 // V: n x n (ld ldv) scratch, set to I here.  offs: max_sweeps zeroed slots.
 // Outputs: sig_out[nv] descending; ut_out row k = column order[k] / sigma;
@@ -67,6 +131,7 @@ __global__ void __launch_bounds__(THREADS) jacobi_grid_kernel(
     int* order, double* sig_out, double* ut_out, int64_t ldut,
     double* vt_out, int64_t ldvt, int* status) {
   cg::grid_group grid = cg::this_grid();
+  __shared__ double red[THREADS / 32];
   const int lane = threadIdx.x & 31;
   const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int nw = (int)((gridDim.x * blockDim.x) >> 5);
@@ -87,7 +152,8 @@ __global__ void __launch_bounds__(THREADS) jacobi_grid_kernel(
     for (int sweep = 0; sweep < max_sweeps; ++sweep) {
       double off = 0.0;
       for (int round = 0; round < n - 1; ++round) {
-        for (int pi = gw; pi < n / 2; pi += nw) {
+        // one CTA per pair: the CTA's warps share the row (block reduce)
+        for (int pi = blockIdx.x; pi < n / 2; pi += gridDim.x) {
           // ring position -> player (dense.py:200-210): position 0 fixed
           auto ring = [&](int pos) -> int {
             if (pos == 0) return 0;
@@ -98,8 +164,8 @@ __global__ void __launch_bounds__(THREADS) jacobi_grid_kernel(
           const int a = ring(pi), b = ring(n - 1 - pi);
           double* xa = W + a * ldw;
           double* xb = W + b * ldw;
-          const double ga = row_dot(xa, xb, len, lane);
           const double al = nrm[a], be = nrm[b];
+          const double ga = block_row_dot(xa, xb, len, red);
           const double den = sqrt(al * be);
           const double rel = den > 0.0 ? fabs(ga) / den : 0.0;
           off = fmax(off, rel);
@@ -110,9 +176,9 @@ __global__ void __launch_bounds__(THREADS) jacobi_grid_kernel(
             const double t = sgn / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
             const double c = 1.0 / sqrt(1.0 + t * t);
             const double s = c * t;
-            row_rotate(xa, xb, len, lane, c, s);
-            if (want_v) row_rotate(V + a * ldv, V + b * ldv, n, lane, c, s);
-            if (lane == 0) {
+            block_row_rotate(xa, xb, len, c, s);
+            if (want_v) block_row_rotate(V + a * ldv, V + b * ldv, n, c, s);
+            if (threadIdx.x == 0) {
               nrm[a] = fmax(al - t * ga, 0.0);
               nrm[b] = fmax(be + t * ga, 0.0);
             }
@@ -120,7 +186,7 @@ __global__ void __launch_bounds__(THREADS) jacobi_grid_kernel(
         }
         grid.sync();
       }
-      if (lane == 0 && off > 0.0) atomicMax(offs + sweep, (unsigned long long)__double_as_longlong(off));
+      if (threadIdx.x == 0 && off > 0.0) atomicMax(offs + sweep, (unsigned long long)__double_as_longlong(off));
       grid.sync();
       sweeps = sweep + 1;
       const double o = __longlong_as_double((long long)*((volatile unsigned long long*)(offs + sweep)));
