@@ -117,14 +117,15 @@ int corutv_decompose_host(corutv_handle* h, const double* a_host, int64_t m, int
 int corutv_jacobi_svd(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda,
                       double* u, double* sigma, double* v);
 
-/* jacobi_svd(a, v_init=...) (dense.py:313-376 warm start): the sweeps start
- * from A_tall v_init, A_tall = a (m >= n) or a' (m < n), and the right
+/* jacobi_svd(a, tol, max_sweeps, v_init) (dense.py:313-376): the sweeps
+ * start from A_tall v_init, A_tall = a (m >= n) or a' (m < n), and the right
  * factor of A_tall is v_init times the rotations.  v_init: k x k device
- * (ld ldvi), orthonormal; NULL = corutv_jacobi_svd.  Replaces
- * _jacobi_svd_tall's v_init branch dense.py:315-321, 352-353. */
+ * (ld ldvi), orthonormal, or NULL (cold start).  tol / max_sweeps: the
+ * stopping rule of dense.py:223-282 (reference defaults 1e-14 / 100).
+ * Replaces _jacobi_svd_tall's v_init branch dense.py:315-321, 352-353. */
 int corutv_jacobi_svd_warm(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda,
-                           const double* v_init, int64_t ldvi, double* u, double* sigma,
-                           double* v);
+                           const double* v_init, int64_t ldvi, double tol, int max_sweeps,
+                           double* u, double* sigma, double* v);
 
 /* Singular value thresholding step of the InexactALM baseline
  * (_svt_warm rpca.py:146-158): warm-started Jacobi SVD of b (m x n), then

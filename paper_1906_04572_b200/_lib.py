@@ -51,7 +51,7 @@ SIGNATURES = {
     "corutv_upload": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _I64]),
     "corutv_download": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _I64]),
     "corutv_jacobi_svd": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _VP, _VP]),
-    "corutv_jacobi_svd_warm": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _I64, _VP, _VP, _VP]),
+    "corutv_jacobi_svd_warm": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _I64, _D, _I32, _VP, _VP, _VP]),
     "corutv_lowrank_error_rank": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _VP, _VP, _I32, _I32, c_double_p]),
     "corutv_qrcp": (_I32, [_VP, _VP, _I64, _I64, _VP, _VP, _VP]),
     "corutv_svt": (_I32, [_VP, _VP, _I64, _I64, _I64, _D, _I32, _VP, _I64, _VP, _VP, _VP, _VP,

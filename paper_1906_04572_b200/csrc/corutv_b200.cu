@@ -710,10 +710,10 @@ void qrcp(corutv_handle* h, const double* D, int l, int64_t ldd, double* T, int6
 // cores that do not fit one CTA's shared memory.  status: device int, set
 // like the one-CTA kernel's (0 ok, 1 no convergence, 2 completion failed).
 void jacobi_grid(corutv_handle* h, const double* X, int nv, int len, int64_t ldx, double* sig_out, int* status,
-                 double* ut, int64_t ldut, double* vt, int64_t ldvt) {
+                 double* ut, int64_t ldut, double* vt, int64_t ldvt, double tol_in, int max_sweeps_in) {
   const int n = nv + (nv > 1 && (nv & 1));
   const int64_t ldw = round_up(len, 2), ldv = round_up(n, 2);
-  constexpr int kMaxSweeps = 100;  // dense.py:36
+  const int kMaxSweeps = std::max(1, max_sweeps_in);
   Arena ar(h);
   double *W, *V = nullptr, *nrm, *sig;
   int *order, *st;
@@ -739,7 +739,7 @@ void jacobi_grid(corutv_handle* h, const double* X, int nv, int len, int64_t ldx
   }();
   // one CTA per column pair of a round
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * h->num_sms, n / 2));
-  double tol = 1e-14;  // dense.py:34
+  double tol = tol_in;
   int max_sweeps = kMaxSweeps, nv_ = nv, n_ = n, len_ = len;
   int64_t ldw_ = ldw, ldv_ = ldv;
   void* args[] = {&W, &ldw_, &V, &ldv_, &nv_, &n_, &len_, &tol, &max_sweeps, &nrm, &offs, &sig, &order, &sig_out,
@@ -756,7 +756,7 @@ void jacobi_grid(corutv_handle* h, const double* X, int nv, int len, int64_t ldx
 // on the cooperative grid.
 void jacobi(corutv_handle* h, const double* X, int nv, int len, int64_t ldx, double* sig, double* pinv,
             int64_t ldp, double* gwork, int* status, double* ut = nullptr, int64_t ldut = 0,
-            double* vt = nullptr, int64_t ldvt = 0) {
+            double* vt = nullptr, int64_t ldvt = 0, double tol = 1e-14, int max_sweeps = 100) {
   const int n = nv + (nv > 1 && (nv & 1));
   const size_t bytes = ((size_t)n * len + ((pinv || vt) ? (size_t)n * n : 0)) * 8;
   const int optin = max_optin_smem(h);
@@ -764,16 +764,16 @@ void jacobi(corutv_handle* h, const double* X, int nv, int len, int64_t ldx, dou
   const bool smem = bytes + stat <= (size_t)optin;
   const int jt = (int)std::min<int64_t>(1024, std::max<int64_t>(64, 32 * (int64_t)((n + 1) / 2)));
   if (!smem && !pinv) {
-    jacobi_grid(h, X, nv, len, ldx, sig, status, ut, ldut, vt, ldvt);
+    jacobi_grid(h, X, nv, len, ldx, sig, status, ut, ldut, vt, ldvt, tol, max_sweeps);
     return;
   }
   if (nv > small::LMAX) fail(h, CORUTV_ERR_ARG, "pseudoinverse core above the supported maximum 640");
   if (smem) {
     set_smem(h, small::jacobi_kernel<true>, bytes);
-    small::jacobi_kernel<true><<<1, jt, bytes, h->stream>>>(X, nv, len, ldx, 1e-14, 100, sig, pinv, ldp, ut, ldut,
+    small::jacobi_kernel<true><<<1, jt, bytes, h->stream>>>(X, nv, len, ldx, tol, max_sweeps, sig, pinv, ldp, ut, ldut,
                                                              vt, ldvt, gwork, 1, status);
   } else {
-    small::jacobi_kernel<false><<<1, jt, 0, h->stream>>>(X, nv, len, ldx, 1e-14, 100, sig, pinv, ldp, ut, ldut,
+    small::jacobi_kernel<false><<<1, jt, 0, h->stream>>>(X, nv, len, ldx, tol, max_sweeps, sig, pinv, ldp, ut, ldut,
                                                           vt, ldvt, gwork, 0, status);
   }
   CK_LAUNCH();
@@ -1759,7 +1759,7 @@ int corutv_decompose_host(corutv_handle* hh, const double* a_host, int64_t m, in
 // (the reference QR-preconditions first; same decomposition to rounding).
 // u: m x k, v: n x k (ld k).  Returns the sweep-count-free status on host.
 void svd_warm(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, const double* v_init,
-              int64_t ldvi, double* u, double* sigma, double* v) {
+              int64_t ldvi, double* u, double* sigma, double* v, double tol = 1e-14, int max_sweeps = 100) {
   const int64_t k = std::min(m, n), len = std::max(m, n);
   const bool tall = m >= n;
   const int64_t ldl = round_up(len, 16), ldk = round_up(k, 16);
@@ -1802,7 +1802,7 @@ void svd_warm(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t l
       run_gemm(h, true, k, n, k, VI, ldk, A, la, X, ldl, nullptr, 0, ws);
     }
   }
-  jacobi(h, X, (int)k, (int)len, ldl, sigma, nullptr, 0, gw, st, UT, ldl, VT, ldk);
+  jacobi(h, X, (int)k, (int)len, ldl, sigma, nullptr, 0, gw, st, UT, ldl, VT, ldk, tol, max_sweeps);
   // right factor of the tall orientation: rotations (rows of VT), times v_init
   const double* R = VT;
   if (v_init) {
@@ -1823,7 +1823,9 @@ void svd_warm(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t l
   sync(h);
   int s0 = 0;
   std::memcpy(&s0, h->pinned, sizeof(int));
-  if (s0 == 1) fail(h, CORUTV_ERR_CONVERGENCE, "one-sided Jacobi did not converge in 100 sweeps");
+  if (s0 == 1)
+    fail(h, CORUTV_ERR_CONVERGENCE,
+         "one-sided Jacobi did not converge in " + std::to_string(max_sweeps) + " sweeps");
   if (s0 == 2) fail(h, CORUTV_ERR_CONVERGENCE, "orthonormal completion ran out of candidates");
 }
 
@@ -1840,13 +1842,15 @@ int corutv_jacobi_svd(corutv_handle* hh, const double* a, int64_t m, int64_t n, 
 }
 
 int corutv_jacobi_svd_warm(corutv_handle* hh, const double* a, int64_t m, int64_t n, int64_t lda,
-                           const double* v_init, int64_t ldvi, double* u, double* sigma, double* v) {
+                           const double* v_init, int64_t ldvi, double tol, int max_sweeps, double* u,
+                           double* sigma, double* v) {
   ABI_BEGIN(hh)
+  if (!(tol >= 0.0) || max_sweeps < 1) fail(h, CORUTV_ERR_ARG, "need tol >= 0 and max_sweeps >= 1");
   if (!a || !u || !sigma || !v) fail(h, CORUTV_ERR_ARG, "null pointer argument");
   if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
   if (std::min(m, n) > kSvdMax) fail(h, CORUTV_ERR_ARG, "jacobi_svd: min(m, n) above the supported maximum 16384");
   if (v_init && ldvi < std::min(m, n)) fail(h, CORUTV_ERR_ARG, "leading dimension of v_init < min(m, n)");
-  svd_warm(h, a, m, n, lda, v_init, ldvi, u, sigma, v);
+  svd_warm(h, a, m, n, lda, v_init, ldvi, u, sigma, v, tol, max_sweeps);
   ABI_END
 }
 

@@ -98,10 +98,8 @@ def jacobi_svd(a, tol: float = JACOBI_TOL, max_sweeps: int = JACOBI_MAX_SWEEPS,
     """dense.py:357-376 on the device: economy SVD by one-sided Jacobi
     (min(m, n) <= 16384; one CTA when the core fits shared memory, else a
     cooperative grid, jacobi_grid.cuh).  ``v_init`` warm-starts the sweeps
-    from the tall orientation's right factor (corutv_jacobi_svd_warm).
-    tol / max_sweeps are fixed at the reference defaults 1e-14 / 100."""
-    if tol != JACOBI_TOL or max_sweeps != JACOBI_MAX_SWEEPS:
-        raise ValueError("jacobi_svd runs with the reference defaults tol=1e-14, max_sweeps=100")
+    from the tall orientation's right factor (corutv_jacobi_svd_warm);
+    exceeding ``max_sweeps`` raises :class:`ConvergenceError`."""
     torch = dev.torch_mod()
     A, was_host = dev.to_device(a, "a")
     dev.raise_if_nonfinite(A, "a")
@@ -112,9 +110,7 @@ def jacobi_svd(a, tol: float = JACOBI_TOL, max_sweeps: int = JACOBI_MAX_SWEEPS,
     s = torch.empty((k,), dtype=torch.float64, device=A.device)
     v = torch.empty((n, k), dtype=torch.float64, device=A.device)
     h = _lib.handle(A.device.index)
-    if V0 is None:
-        h.call("corutv_jacobi_svd", dev.ptr(A), m, n, A.stride(0), dev.ptr(u), dev.ptr(s), dev.ptr(v))
-    else:
-        h.call("corutv_jacobi_svd_warm", dev.ptr(A), m, n, A.stride(0), dev.ptr(V0), V0.stride(0),
-               dev.ptr(u), dev.ptr(s), dev.ptr(v))
+    h.call("corutv_jacobi_svd_warm", dev.ptr(A), m, n, A.stride(0), dev.ptr(V0) if V0 is not None else None,
+           V0.stride(0) if V0 is not None else 0, float(tol), int(max_sweeps), dev.ptr(u), dev.ptr(s),
+           dev.ptr(v))
     return SvdFactors(u=dev.to_output(u, was_host), sigma=dev.to_output(s, was_host), v=dev.to_output(v, was_host))

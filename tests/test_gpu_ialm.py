@@ -172,3 +172,17 @@ def test_inexact_alm_desk_scale_golden(golden):
     assert np.abs(sol.l[::37, ::41] - c["l_sample"]).max() <= 1e-8 * np.abs(m).max()
     assert np.linalg.norm(sol.l - l_true) <= 1e-4 * np.linalg.norm(l_true)
     assert dt < 60.0  # the reference's own desk-scale budget (test_acceptance.py:262-270)
+
+
+@pytest.mark.parametrize("n", [40, 300])
+def test_jacobi_svd_sweep_cap_and_tolerance(n):
+    # dense.py:357-376 arguments: max_sweeps exceeded -> ConvergenceError
+    # (one-CTA path for n = 40, grid path for n = 300); a looser tol stops
+    # earlier with the spectrum still right to ~tol
+    g = np.random.Generator(np.random.PCG64(n))
+    a = g.standard_normal((n, n))
+    with pytest.raises(P.ConvergenceError, match="did not converge"):
+        P.jacobi_svd(a, max_sweeps=1)
+    f = P.jacobi_svd(a, tol=1e-8)
+    s = O.jacobi_svd(a)[1]
+    assert np.abs(f.sigma - s).max() <= 1e-6 * s[0]
