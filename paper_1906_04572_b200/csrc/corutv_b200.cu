@@ -918,7 +918,7 @@ void svd_lift(corutv_handle* h, const double* C, int l, int64_t ldp, const doubl
   sync(h);
   int st = 0;
   std::memcpy(&st, h->pinned, sizeof(int));
-  if (st == 1) fail(h, CORUTV_ERR_CONVERGENCE, "one-sided Jacobi did not converge in 100 sweeps");
+  if (st == 1) fail(h, CORUTV_ERR_CONVERGENCE, "one-sided Jacobi did not converge in 100 sweeps; relative off-diagonal residual exceeds 1.0e-14");
   if (st == 2) fail(h, CORUTV_ERR_CONVERGENCE, "orthonormal completion ran out of candidates");
 }
 
@@ -1506,7 +1506,7 @@ void singular_values(corutv_handle* h, const double* a, int64_t m, int64_t n, in
   CK(cudaMemcpyAsync(h->pinned, st, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   sync(h);
   if (*reinterpret_cast<int*>(h->pinned))
-    fail(h, CORUTV_ERR_CONVERGENCE, "one-sided Jacobi did not converge in 100 sweeps");
+    fail(h, CORUTV_ERR_CONVERGENCE, "one-sided Jacobi did not converge in 100 sweeps; relative off-diagonal residual exceeds 1.0e-14");
 }
 
 // |A|_2, dense.py:405-442.
@@ -1825,7 +1825,8 @@ void svd_warm(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t l
   std::memcpy(&s0, h->pinned, sizeof(int));
   if (s0 == 1)
     fail(h, CORUTV_ERR_CONVERGENCE,
-         "one-sided Jacobi did not converge in " + std::to_string(max_sweeps) + " sweeps");
+         "one-sided Jacobi did not converge in " + std::to_string(max_sweeps) +
+             " sweeps; relative off-diagonal residual exceeds tol " + std::to_string(tol));
   if (s0 == 2) fail(h, CORUTV_ERR_CONVERGENCE, "orthonormal completion ran out of candidates");
 }
 
