@@ -100,18 +100,12 @@ __device__ double upper_sumsq(const double* W, int l, int ld, int col0, bool low
 // first and keep it when it succeeds with kappa_F <= kappa_max.
 // Output rinvT (l x l, ld ldr): rinvT[j][k] = R^-1[k][j] (the Bt operand of
 // the X * R^-1 GEMM).  Work: [G | I], 2 l^2 doubles of shared memory.
-__global__ void __launch_bounds__(512, 1)
-    chol_factor_kernel(const double* __restrict__ G, int l, int64_t ldg, double shift_coeff,
-                       int allow_plain, double kappa_max, double* __restrict__ rinvT,
-                       int64_t ldr, double* gwork, int use_smem, CholInfo* info) {
-  extern __shared__ double dsm[];
-  __shared__ double red[NWARPS];
-  // [G | I] always in shared memory here (the host launches this kernel only
-  // when it fits; larger cores use the cluster kernel), so every access is
-  // an LDS/STS rather than a generic LD/ST
-  (void)use_smem;
-  (void)gwork;
-  double* W = dsm;
+// The factorisation itself, for one whole CTA (any block size) with W =
+// 2 l^2 doubles and red = NWARPS doubles of shared memory; also called by
+// the fused tall-skinny CholeskyQR (skinny.cuh).
+__device__ void chol_factor_block(const double* G, int l, int64_t ldg, double shift_coeff, int allow_plain,
+                                  double kappa_max, double* rinvT, int64_t ldr, CholInfo* info, double* W,
+                                  double* red) {
   const int ld = 2 * l;
   double tr = 0.0;
   for (int i = threadIdx.x; i < l; i += blockDim.x) tr += G[i * ldg + i];
@@ -164,6 +158,20 @@ __global__ void __launch_bounds__(512, 1)
     info->kappa = kappa;
     info->trace = tr;
   }
+}
+
+__global__ void __launch_bounds__(512, 1)
+    chol_factor_kernel(const double* __restrict__ G, int l, int64_t ldg, double shift_coeff,
+                       int allow_plain, double kappa_max, double* __restrict__ rinvT,
+                       int64_t ldr, double* gwork, int use_smem, CholInfo* info) {
+  extern __shared__ double dsm[];
+  __shared__ double red[NWARPS];
+  // [G | I] always in shared memory here (the host launches this kernel only
+  // when it fits; larger cores use the cluster kernel), so every access is
+  // an LDS/STS rather than a generic LD/ST
+  (void)use_smem;
+  (void)gwork;
+  chol_factor_block(G, l, ldg, shift_coeff, allow_plain, kappa_max, rinvT, ldr, info, dsm, red);
 }
 
 // ------------------------------------------------------------------- QRCP
