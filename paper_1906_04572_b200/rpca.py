@@ -25,7 +25,7 @@ from . import _device as dev
 from . import _lib
 from .dense import singular_values, spectral_norm
 from .errors import ConvergenceError
-from .sketch import SketchConfig, corutv, corutv_truncated
+from .sketch import SketchConfig, corutv, corutv_truncated  # noqa: F401  (rpca.corutv, as in the reference module)
 
 __all__ = [
     "AlmConfig",
