@@ -59,6 +59,11 @@ struct corutv_handle {
   unsigned char* tails = nullptr;
   int tails_cap = 0;
   cudaEvent_t est_ev = nullptr;  // spectral norm: readiness of the async estimate
+  // second compute stream: the two sketches' CholeskyQR steps run side by
+  // side (a cluster Cholesky occupies 8-16 SMs; the other job's GEMMs fill
+  // the rest)
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   // profiling (corutv_profile_begin/end): launch counter always on; CUDA
   // events around the DMMA GEMM / low-rank kernels while enabled.
   int64_t launches = 0;
@@ -599,22 +604,45 @@ void cholqr_multi(corutv_handle* h, QrJob* jobs, int njobs, int ell, int64_t ldx
                           kKappaPlain, q.w.rinvT, ldx, q.w.gwork, q.w.info));
     ++h->launches;
   };
+  auto run_step = [&](QrJob& q, int j) {
+    const double coeff = 11.0 * (q.rows_global * l + (double)l * (l + 1)) * kUnit;
+    run_gemm(h, true, l, l, q.rows, q.cur, ldx, q.cur, ldx, q.w.G, ldx, nullptr, 0, q.w.ws);
+    if (q.sharded) allreduce(h, q.w.G, (int64_t)l * ldx);
+    launch_factor(q, coeff);
+    run_gemm(h, false, q.rows, l, l, q.cur, ldx, q.w.rinvT, ldx, q.nxt, ldx, nullptr, 0, q.w.ws);
+    std::swap(q.cur, q.nxt);
+    CK(cudaMemcpyAsync(h->pinned + 4 * j, q.w.info, sizeof(small::CholInfo), cudaMemcpyDeviceToHost, h->stream));
+  };
+  // two independent unsharded jobs with their own split-K scratch: job 1 on
+  // the side stream, job 0 on the caller's (same kernels, same results)
+  const bool pair = njobs == 2 && jobs[0].w.ws != jobs[1].w.ws && !jobs[0].sharded && !jobs[1].sharded;
+  if (pair && !h->side) {
+    CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->join_ev, cudaEventDisableTiming));
+  }
   for (int step = 0; step < kMaxQrSteps; ++step) {
     int active = 0;
-    for (int j = 0; j < njobs; ++j) {
-      QrJob& q = jobs[j];
-      if (q.done) continue;
-      ++active;
-      const double coeff = 11.0 * (q.rows_global * l + (double)l * (l + 1)) * kUnit;
-      run_gemm(h, true, l, l, q.rows, q.cur, ldx, q.cur, ldx, q.w.G, ldx, nullptr, 0, q.w.ws);
-      if (q.sharded) allreduce(h, q.w.G, (int64_t)l * ldx);
-      launch_factor(q, coeff);
-      run_gemm(h, false, q.rows, l, l, q.cur, ldx, q.w.rinvT, ldx, q.nxt, ldx, nullptr, 0, q.w.ws);
-      std::swap(q.cur, q.nxt);
-      CK(cudaMemcpyAsync(h->pinned + 4 * j, q.w.info, sizeof(small::CholInfo), cudaMemcpyDeviceToHost,
-                         h->stream));
-    }
+    for (int j = 0; j < njobs; ++j) active += jobs[j].done ? 0 : 1;
     if (!active) return;
+    if (pair && active == 2) {
+      CK(cudaEventRecord(h->fork_ev, h->stream));
+      CK(cudaStreamWaitEvent(h->side, h->fork_ev, 0));
+      struct StreamSwap {
+        corutv_handle* h;
+        cudaStream_t saved;
+        ~StreamSwap() { h->stream = saved; }
+      } swap{h, h->stream};
+      h->stream = h->side;
+      run_step(jobs[1], 1);
+      CK(cudaEventRecord(h->join_ev, h->side));
+      h->stream = swap.saved;
+      run_step(jobs[0], 0);
+      CK(cudaStreamWaitEvent(h->stream, h->join_ev, 0));
+    } else {
+      for (int j = 0; j < njobs; ++j)
+        if (!jobs[j].done) run_step(jobs[j], j);
+    }
     if (step == 0 && extra_flag)
       CK(cudaMemcpyAsync(h->pinned + 60, extra_flag, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     sync(h);
@@ -1103,6 +1131,9 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   wse = std::max(wse, gemm_ws_elems(h, l, l, m));
   wse = std::max(wse, gemm_ws_elems(h, l, l, n));
   ar.add(&ws, wse + 16);
+  // split-K scratch of the C2 sketch's CholeskyQR (runs beside the C1 one)
+  double* ws_qr2 = nullptr;
+  if (!sharded) ar.add(&ws_qr2, std::max(gemm_ws_elems(h, l, l, n), gemm_ws_elems(h, n, l, l)) + 16);
   // host input: the first A' C1 sweep runs split by split as row chunks land
   const GemmPlan k2plan = plan_gemm(h, n, l, m, true);
   double* ws2 = nullptr;
@@ -1201,7 +1232,7 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   jobs[1].rows = n;
   jobs[1].rows_global = (double)n;
   jobs[1].sharded = false;
-  jobs[1].w = QrWork{G2, rinvT2, gwork2, ws, info + 2};
+  jobs[1].w = QrWork{G2, rinvT2, gwork2, ws_qr2 ? ws_qr2 : ws, info + 2};
   cholqr_multi(h, jobs, 2, l, ldp, flagd);
   double* Q1 = jobs[0].cur;
   double* Q2 = jobs[1].cur;
@@ -1731,6 +1762,12 @@ void corutv_destroy(corutv_handle* h) {
   if (h->tails) cudaFreeHost(h->tails);
   if (h->est_ev) cudaEventDestroy(h->est_ev);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  if (h->side) {
+    cudaStreamSynchronize(h->side);
+    cudaStreamDestroy(h->side);
+  }
+  if (h->fork_ev) cudaEventDestroy(h->fork_ev);
+  if (h->join_ev) cudaEventDestroy(h->join_ev);
   delete h;
 }
 
