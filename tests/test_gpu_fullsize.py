@@ -70,3 +70,38 @@ def test_c5_full_size_properties():
     assert 0.8 * tail <= err <= 1.25 * tail
     assert abs(float(d[0]) - 0.99) < 0.1
     del a, f
+
+
+def test_c4_full_size_matches_oracle_histories():
+    # BASELINE configs[3] (C4, n = 10000): the ALM run on the device against
+    # the CPU oracle's recorded run on the same M (tests/golden/c4_oracle.json,
+    # tools/c4_parity.py): same mu0, identical iteration count and
+    # cap / rank / nnz histories, residual to rounding; the device spectral
+    # norm against the oracle's
+    import json
+    from pathlib import Path
+
+    ref = json.loads((Path(__file__).parent / "golden" / "c4_oracle.json").read_text())
+    dev = torch.device("cuda", 0)
+    n, k = 10000, 50
+    g = torch.Generator(device=dev)
+    g.manual_seed(777)
+    x = torch.randn((n, k), generator=g, dtype=torch.float64, device=dev) / 100.0
+    y = torch.randn((n, k), generator=g, dtype=torch.float64, device=dev) / 100.0
+    mat = x @ y.T
+    nnz = n * n // 20
+    pos = torch.randperm(n * n, generator=g, device=dev)[:nnz]
+    vals = (torch.rand((nnz,), generator=g, dtype=torch.float64, device=dev) * 1000.0) - 500.0
+    mat.view(-1)[pos] += vals
+    s, it = P.dense.spectral_norm_iters(mat)
+    assert abs(s - ref["spectral_norm"]) <= 1e-12 * ref["spectral_norm"]
+    assert abs(it - ref["spectral_norm_iters"]) <= 1
+    cfg = P.AlmConfig(ell=2 * k, lam=1 / math.sqrt(n), tol=1e-7, q_power=1, seed=0,
+                      mu0=1.25 / ref["spectral_norm"])
+    sol = P.alm_corutv(mat, cfg)
+    assert sol.iterations == ref["iterations"]
+    assert sol.ell_history == ref["ell_history"]
+    assert sol.rank_history == ref["rank_history"]
+    assert sol.rank_of_l == ref["rank_of_l"] and sol.nnz_of_s == ref["nnz_of_s"]
+    assert abs(sol.residuals[-1] - ref["final_residual"]) <= 1e-6 * ref["final_residual"]
+    del mat, sol
