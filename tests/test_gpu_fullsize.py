@@ -105,3 +105,38 @@ def test_c4_full_size_matches_oracle_histories():
     assert sol.rank_of_l == ref["rank_of_l"] and sol.nnz_of_s == ref["nnz_of_s"]
     assert abs(sol.residuals[-1] - ref["final_residual"]) <= 1e-6 * ref["final_residual"]
     del mat, sol
+
+
+def test_c3_full_size_matches_oracle():
+    # BASELINE configs[2] at full size against the CPU oracle on the same A
+    # and seeded Omega (tools/c3_parity.py; ~30 s of 16-core oracle time and
+    # ~36 GB of host memory)
+    import numpy as np
+    import psutil
+
+    import oracle as O
+
+    if psutil.virtual_memory().available < 80 * 2 ** 30:
+        pytest.skip("needs ~36 GB of free host memory for the oracle copy of A")
+    m, n, ell, q, k, noise, _ = bench.WORKLOADS["c3"]
+    a = bench.gen_rows_device(torch, "c3", 0, m, torch.device("cuda", 0))
+    f = P.corutv(a, P.SketchConfig(ell=ell, q_power=q, seed=0))
+    a_host = a.cpu().numpy()
+    ref = O.corutv(a_host, ell, q, seed=0)
+    del a_host
+    d_dev = f.t.diagonal().abs().cpu().numpy()
+    d_ref = np.abs(np.diag(ref["t"]))
+    assert np.abs(d_dev[:k] - d_ref[:k]).max() <= 1e-12 * d_ref[0]
+    assert np.array_equal(np.asarray(f.perm.cpu())[:k], ref["perm"][:k])
+    u, v = f.u[:, :k].cpu().numpy(), f.v[:, :k].cpu().numpy()
+    su = np.sign(np.sum(u * ref["u"][:, :k], axis=0))
+    sv = np.sign(np.sum(v * ref["v"][:, :k], axis=0))
+    assert np.abs(u * su - ref["u"][:, :k]).max() <= 1e-10
+    assert np.abs(v * sv - ref["v"][:, :k]).max() <= 1e-10
+    e_dev = P.corutv_lowrank_error(a, P.SketchConfig(ell=ell, q_power=q, seed=0))
+    # |A - U T V'| of the oracle's factors from the exact-d identity
+    # |A|^2 = |A - U T V'|^2 + |T|^2 (U T V' = P1 A P2)
+    a2 = float(P.dense.frobenius_norm(a)) ** 2
+    e_ref = math.sqrt(max(a2 - float((ref["t"] ** 2).sum()), 0.0))
+    assert abs(e_dev - e_ref) <= 1e-8 * e_ref
+    del a, f
