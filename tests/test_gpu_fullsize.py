@@ -109,7 +109,7 @@ def test_c4_full_size_matches_oracle_histories():
 
 def test_c3_full_size_matches_oracle():
     # BASELINE configs[2] at full size against the CPU oracle on the same A
-    # and seeded Omega (tools/c3_parity.py; ~30 s of 16-core oracle time and
+    # and seeded Omega (tools/full_parity.py; ~30 s of 16-core oracle time and
     # ~36 GB of host memory)
     import numpy as np
     import psutil
