@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(THREADS) cholqr_kernel(const double* x0, int64
                                                          double* rinvT, small::CholInfo* info, double* q,
                                                          int64_t ldq, double* qT, int64_t ldqT, int* status) {
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ double xs[];  // this CTA's rows, chunk x b
+  extern __shared__ __align__(16) double xs[];  // this CTA's rows, chunk x b
   __shared__ double W[2 * BMAX * BMAX];
   __shared__ double red[small::NWARPS];
   __shared__ double R[BMAX * BMAX];
