@@ -120,3 +120,38 @@ def test_pass_counter():
     c.add()
     c.add(4)
     assert c.passes == 5
+
+
+def test_install_rebinds_the_next_rows():
+    # sor_svd / tsr_svd / inexact_alm / svt are rebound where the reference
+    # package defines them (sketch.py:220-262, rpca.py:135-158, 258-273)
+    import sys
+
+    pkg = types.ModuleType("fakecorutv2")
+    pkg.__path__ = []
+    pkg.inexact_alm = pkg.svt = pkg.sor_svd = object()
+    mods = {}
+    for sub in ("sketch", "rpca", "bench"):
+        m = types.ModuleType(f"fakecorutv2.{sub}")
+        m.corutv = object()
+        if sub == "sketch":
+            m.sor_svd = m.tsr_svd = object()
+        else:
+            m.alm_corutv = m.inexact_alm = object()
+        if sub == "rpca":
+            m.svt = object()
+        mods[sub] = m
+        sys.modules[f"fakecorutv2.{sub}"] = m
+    sys.modules["fakecorutv2"] = pkg
+    try:
+        done = P.install(pkg)
+        assert mods["sketch"].sor_svd is P.sor_svd and mods["sketch"].tsr_svd is P.tsr_svd
+        assert mods["rpca"].inexact_alm is P.inexact_alm and mods["rpca"].svt is P.svt
+        assert mods["bench"].inexact_alm is P.inexact_alm
+        assert pkg.inexact_alm is P.inexact_alm and pkg.svt is P.svt and pkg.sor_svd is P.sor_svd
+        assert not hasattr(pkg, "tsr_svd")
+        assert "fakecorutv2.rpca.inexact_alm" in done
+    finally:
+        for k in list(sys.modules):
+            if k.startswith("fakecorutv2"):
+                del sys.modules[k]
