@@ -1,7 +1,7 @@
 """Full-size C3 / C5 parity (BASELINE configs[2]: 131072 x 32768, ell 110,
 q 2; configs[4]: 262144 x 32768, ell 272, q 2) against the CPU oracle, on the
 GPU box (oracle: numpy restatement of sketch.py:166-208 on 16 cores; ~36 /
-~72 GB of host memory).  usage: full_parity.py [c3|c5]
+~72 GB of host memory).  usage: full_parity.py [c3|c5] [exact-d|approx-d]
 
 Same A for both (bench.gen_rows_device, copied to the host) and the same
 seeded Omega (the device draws numpy's PCG64 stream bit-identically).
@@ -27,16 +27,17 @@ from paper_1906_04572_b200 import _lib
 torch.cuda.set_device(0)
 dev = torch.device("cuda", 0)
 wl = sys.argv[1] if len(sys.argv) > 1 else "c3"
+variant = sys.argv[2] if len(sys.argv) > 2 else "exact-d"
 m, n, ell, q, k, noise, _ = bench.WORKLOADS[wl]
 a = bench.gen_rows_device(torch, wl, 0, m, dev)
 torch.cuda.synchronize()
 t0 = time.perf_counter()
-f = P.corutv(a, P.SketchConfig(ell=ell, q_power=q, seed=0))
+f = P.corutv(a, P.SketchConfig(ell=ell, q_power=q, seed=0, variant=variant))
 torch.cuda.synchronize()
-out = {"workload": wl, "device_s": time.perf_counter() - t0}
+out = {"workload": wl, "variant": variant, "device_s": time.perf_counter() - t0}
 a_host = a.cpu().numpy()
 t0 = time.perf_counter()
-ref = O.corutv(a_host, ell, q, seed=0)
+ref = O.corutv(a_host, ell, q, seed=0, variant=variant)
 out["oracle_s"] = time.perf_counter() - t0
 del a_host
 
@@ -70,4 +71,5 @@ out.update({
     "passes_oracle": ref["passes"],
 })
 print(json.dumps(out, indent=1))
-json.dump(out, open(f"gpurun_out/{wl}_parity.json", "w"), indent=1)
+tag = "" if variant == "exact-d" else "_approx"
+json.dump(out, open(f"gpurun_out/{wl}{tag}_parity.json", "w"), indent=1)
