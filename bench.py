@@ -457,6 +457,8 @@ def main():
     rpca = None
     if not args.no_rpca and world == 1:
         rpca = bench_rpca(torch, P, device)
+    elif not args.no_rpca:
+        rpca = bench_rpca(torch, P, device, world, rank, tdist, comm)
 
     # ------------------------------------------------------------- CPU leg
     cpu = None
@@ -504,11 +506,13 @@ def main():
     return 0
 
 
-def bench_rpca(torch, P, device):
+def bench_rpca(torch, P, device, world=1, rank=0, tdist=None, comm=None):
     """BASELINE configs[3] (C4): M = X Y' + S, n = 10000, X, Y 10000 x 50
     N(0, 1/10000), 5% spikes U[-500, 500] at uniform positions; lam =
     1/sqrt(n), tol = 1e-7, ell0 = 2k = 100, q = 1.  mu0 = 1.25/|M|_2 is
-    timed separately (spectral_norm) and passed in."""
+    timed separately (spectral_norm) and passed in.  world > 1: M row-sharded
+    over the ranks (dist.alm_corutv_sharded; every rank builds the same M and
+    keeps its rows), wall time the max over ranks."""
     n, k = 10000, 50
     g = torch.Generator(device=device)
     g.manual_seed(777)
@@ -520,25 +524,55 @@ def bench_rpca(torch, P, device):
     vals = (torch.rand((nnz,), generator=g, dtype=torch.float64, device=device) * 1000.0) - 500.0
     mat.view(-1)[pos] += vals
     del x, y, pos, vals
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    snorm, sit = P.dense.spectral_norm_iters(mat)
-    t_snorm = time.perf_counter() - t0
-    cfg = P.AlmConfig(lam=1 / math.sqrt(n), tol=1e-7, ell=2 * k, q_power=1, seed=0, mu0=1.25 / snorm)
+    if world > 1:
+        from paper_1906_04572_b200.dist import alm_corutv_sharded, row_range
+
+        lo, hi = row_range(n, world, rank)
+        mat = mat[lo:hi].contiguous()
+        h = P._lib.handle(device.index)
+        comm.attach(h)
+        try:
+            torch.cuda.synchronize()
+            tdist.barrier()
+            t0 = time.perf_counter()
+            snorm, sit = P.dense.spectral_norm_iters(mat)
+            t_snorm = time.perf_counter() - t0
+        finally:
+            comm.detach(h)
+        cfg = P.AlmConfig(lam=1 / math.sqrt(n), tol=1e-7, ell=2 * k, q_power=1, seed=0, mu0=1.25 / snorm)
+
+        def solve():
+            return alm_corutv_sharded(mat, cfg, comm, n)
+    else:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        snorm, sit = P.dense.spectral_norm_iters(mat)
+        t_snorm = time.perf_counter() - t0
+        cfg = P.AlmConfig(lam=1 / math.sqrt(n), tol=1e-7, ell=2 * k, q_power=1, seed=0, mu0=1.25 / snorm)
+
+        def solve():
+            return P.alm_corutv(mat, cfg)
     # warm-up solve (lazy kernel loading, workspace growth), then the timed one
-    P.alm_corutv(mat, cfg)
+    solve()
     torch.cuda.synchronize()
+    if world > 1:
+        tdist.barrier()
     t0 = time.perf_counter()
-    sol = P.alm_corutv(mat, cfg)
+    sol = solve()
     torch.cuda.synchronize()
     t_alm = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([t_alm, t_snorm], dtype=torch.float64, device=device)
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+        t_alm, t_snorm = float(tt[0]), float(tt[1])
     out = {"workload": "c4", "n": n, "ms_per_iter": round(1e3 * t_alm / sol.iterations, 3),
            "iterations": sol.iterations, "alm_total_s": round(t_alm, 3),
            "spectral_norm_s": round(t_snorm, 3), "spectral_norm_iters": sit,
            "rank_of_l": sol.rank_of_l, "nnz_of_s": sol.nnz_of_s,
            "final_residual": sol.residuals[-1], "ell_history": sol.ell_history,
+           "ranks": world,
            "timing": "wall clock around alm_corutv (host decisions included), sync on both sides, "
-                     "after one untimed warm-up solve"}
+                     "after one untimed warm-up solve" + ("; row-sharded, max over ranks" if world > 1 else "")}
     del mat, sol
     torch.cuda.empty_cache()
     return out

@@ -25,7 +25,7 @@ from . import _device as dev
 from . import _lib
 from .sketch import _VARIANT_CODE, CorUtvFactors, PassCounter, SketchConfig, pcg_state
 
-__all__ = ["row_range", "RowShardComm", "corutv_sharded"]
+__all__ = ["row_range", "RowShardComm", "corutv_sharded", "alm_corutv_sharded"]
 
 
 def row_range(m: int, world: int, rank: int) -> tuple[int, int]:
@@ -126,3 +126,35 @@ def corutv_sharded(a_local, cfg: SketchConfig, comm: RowShardComm, counter: Pass
     return CorUtvFactors(u=dev.to_output(u, was_host), t=dev.to_output(t, was_host),
                          v=dev.to_output(v, was_host), ell=ell, q_power=cfg.q_power,
                          variant=cfg.variant, perm=dev.to_output(perm, was_host))
+
+
+def alm_corutv_sharded(m_local, cfg, comm: RowShardComm, global_rows: int):
+    """alm_corutv (rpca.py:237-255) of the row-sharded global M whose rows
+    ``row_range(global_rows, world, rank)`` are ``m_local`` on this rank
+    (BASELINE configs[3] "on 1 and 8 GPUs").  Every exchange is inside the
+    library: |M|_F and the spectral norm (mu0), the sketch products and
+    Grams of each CoR-UTV, and the residual / support counts of the fused
+    update are all-reduced, so the scalar decisions (rank, cap, mu, stop)
+    are identical on all ranks.  Returns this rank's rows of L and S and the
+    replicated histories."""
+    from . import rpca
+
+    if cfg.ell is None:
+        raise ValueError("alm_corutv requires cfg.ell (sketch sample size)")
+    A, _ = dev.to_device(m_local, "m")
+    h = _lib.handle(A.device.index)
+    comm.attach(h)
+    try:
+        def step(g, delta, cap, j, state):
+            scfg = SketchConfig(ell=cap, q_power=cfg.q_power, seed=(cfg.seed + j) % 2 ** 64)
+            f, rank = rpca.corutv_truncated(g, scfg, delta)
+
+            def sigma_of():
+                sig = rpca.singular_values(f.t[:rank, :])
+                return sig.cpu().numpy() if dev.is_device_tensor(sig) else sig
+
+            return f.u, f.t, f.v, f.ell, rank, sigma_of, None
+
+        return rpca._alm_loop(m_local, cfg, step, cap0=cfg.ell, global_rows=global_rows)
+    finally:
+        comm.detach(h)

@@ -177,7 +177,7 @@ def svt(b, delta: float):
     return dev.to_output(_lowrank_device(u, t, v, r), was_host), r
 
 
-def _alm_loop(m, cfg: AlmConfig, step, cap0) -> RpcaSolution:
+def _alm_loop(m, cfg: AlmConfig, step, cap0, global_rows: int | None = None) -> RpcaSolution:
     """rpca.py:175-234 on the device.  ``step(g, delta, cap, j, state)``
     returns (u, t, v, ell, rank, sigma_thunk, state): the thresholded iterate
     is u[:, :rank] (t[:rank, :] v'), kept implicit and fused into the ALM
@@ -187,9 +187,10 @@ def _alm_loop(m, cfg: AlmConfig, step, cap0) -> RpcaSolution:
     M, was_host = dev.to_device(m, "m")
     if M.stride(0) != M.shape[1]:
         M = M.contiguous()
-    h_, w_ = M.shape
+    h_, w_ = M.shape           # local block (all rows unless row-sharded)
+    hg = global_rows if global_rows is not None else h_
     handle = _lib.handle(M.device.index)
-    lam = cfg.lam if cfg.lam is not None else 1.0 / np.sqrt(max(h_, w_))
+    lam = cfg.lam if cfg.lam is not None else 1.0 / np.sqrt(max(hg, w_))
     ss = ctypes.c_double(0.0)
     handle.call("corutv_sumsq", dev.ptr(M), h_, w_, M.stride(0), ctypes.byref(ss))
     if not math.isfinite(ss.value):
@@ -202,7 +203,7 @@ def _alm_loop(m, cfg: AlmConfig, step, cap0) -> RpcaSolution:
                             rank_history=[0], nnz_history=[0], mu_history=[0.0], ell_history=[0])
     mu = cfg.mu0 if cfg.mu0 is not None else 1.25 / spectral_norm(M)
     mu_bar = cfg.mu_bar if cfg.mu_bar is not None else 1e7 * mu
-    limit = min(h_, w_)
+    limit = min(hg, w_)
     grow = max(1, round(0.05 * limit))
     cap = max(1, min(cap0 if cap0 is not None else limit, limit))
     y = torch.zeros_like(M)
@@ -236,7 +237,7 @@ def _alm_loop(m, cfg: AlmConfig, step, cap0) -> RpcaSolution:
                 sig = np.zeros(0)
             return RpcaSolution(
                 l=dev.to_output(l_mat, was_host), s=dev.to_output(s, was_host), iterations=j + 1,
-                residuals=residuals, rank_of_l=_numerical_rank(sig, (h_, w_)),
+                residuals=residuals, rank_of_l=_numerical_rank(sig, (hg, w_)),
                 nnz_of_s=int(nnz.value), rank_history=ranks, nnz_history=nnzs, mu_history=mus,
                 ell_history=caps,
             )
