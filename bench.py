@@ -458,7 +458,10 @@ def main():
     if not args.no_rpca and world == 1:
         rpca = bench_rpca(torch, P, device)
     elif not args.no_rpca:
-        rpca = bench_rpca(torch, P, device, world, rank, tdist, comm)
+        try:
+            rpca = bench_rpca(torch, P, device, world, rank, tdist, comm)
+        except Exception as exc:  # the headline line must still print
+            rpca = {"workload": "c4", "ranks": world, "error": str(exc)[:200]}
 
     # ------------------------------------------------------------- CPU leg
     cpu = None
