@@ -2,8 +2,12 @@
 import sys
 import time
 sys.path.insert(0, '.')
+import os
+from pathlib import Path
 import torch
 import paper_1906_04572_b200 as P
+if os.environ.get("CORUTV_LIB"):  # A/B a variant build of the library
+    P._lib.LIB_PATH = Path(os.environ["CORUTV_LIB"]).resolve()
 
 torch.cuda.set_device(0)
 for n in [int(x) for x in sys.argv[1:]] or [400, 1000]:
