@@ -141,8 +141,9 @@ def alm_corutv_sharded(m_local, cfg, comm: RowShardComm, global_rows: int):
 
     if cfg.ell is None:
         raise ValueError("alm_corutv requires cfg.ell (sketch sample size)")
-    A, _ = dev.to_device(m_local, "m")
-    h = _lib.handle(A.device.index)
+    torch = dev.torch_mod()
+    device = m_local.device.index if dev.is_device_tensor(m_local) else torch.cuda.current_device()
+    h = _lib.handle(device)
     comm.attach(h)
     try:
         def step(g, delta, cap, j, state):
