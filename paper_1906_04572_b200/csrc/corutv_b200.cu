@@ -1640,7 +1640,7 @@ void spectral_norm(corutv_handle* h, const double* a, int64_t m, int64_t n, int6
     // est = sigma_1(w) = sqrt(lambda_max(w'w))
     run_gemm(h, true, b, b, mp, w, ldb2, w, ldb2, G, ldb2, nullptr, 0, ws);
     if (sharded) allreduce(h, G, (int64_t)b * ldb2);
-    small::sym_lmax_kernel<<<1, 32, 0, h->stream>>>(G, b, ldb2, sig);
+    small::sym_lmax_kernel<<<1, small::LMAX_THREADS, 0, h->stream>>>(G, b, ldb2, sig);
     CK_LAUNCH();
     // the estimate comes back asynchronously: the next product and its QR
     // are queued before the host looks at it (their synchronisations make it

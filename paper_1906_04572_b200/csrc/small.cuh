@@ -568,23 +568,36 @@ __global__ void __launch_bounds__(THREADS, 1)
 // lambda_max is accurate to a few u ||G|| -- what the block power iteration
 // of spectral_norm needs from sigma_1(w)^2 = lambda_max(w'w) (dense.py:425-431
 // takes sigma_1 of the QR factor of w; same value to rounding).
-__global__ void __launch_bounds__(32) sym_lmax_kernel(const double* __restrict__ G, int b, int64_t ldg,
-                                                      double* __restrict__ out) {
+constexpr int LMAX_THREADS = 256;
+
+__global__ void __launch_bounds__(LMAX_THREADS) sym_lmax_kernel(const double* __restrict__ G, int b, int64_t ldg,
+                                                                double* __restrict__ out) {
+  // 8 warps: rows of the Householder updates are spread over the warps
+  // (warp w owns rows i = w mod 8), and the multisection evaluates 256
+  // shifts per step (8 bits) instead of 32
   __shared__ double A[32][33];
-  __shared__ double vs[32], ws[32], d[32], e[32];
-  const int lane = threadIdx.x;
-  for (int j = 0; j < b; ++j)
-    if (lane < b) A[lane][j] = (lane >= j) ? G[lane * ldg + j] : G[j * ldg + lane];
-  __syncwarp();
+  __shared__ double ps[32], d[32], e[32];
+  __shared__ double xs[LMAX_THREADS];
+  __shared__ int cs[LMAX_THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = LMAX_THREADS / 32;
+  for (int idx = tid; idx < b * b; idx += LMAX_THREADS) {
+    const int i = idx / b, j = idx % b;
+    A[i][j] = (i >= j) ? G[i * ldg + j] : G[j * ldg + i];
+  }
+  __syncthreads();
   for (int k = 0; k + 2 < b; ++k) {
     // reflector for x = A[k+1:b, k]:  H x = beta e1, H = I - tau v v', v[0] = 1
+    // (every warp forms the same scalars and v from shared memory)
     const double alpha = A[k + 1][k];
     const double xt = (lane > k + 1 && lane < b) ? A[lane][k] : 0.0;
     const double sigma = warp_sum(xt * xt);
-    d[k] = A[k][k];
     if (sigma == 0.0) {
-      if (lane == 0) e[k] = alpha;
-      __syncwarp();
+      if (tid == 0) {
+        d[k] = A[k][k];
+        e[k] = alpha;
+      }
+      __syncthreads();
       continue;
     }
     const double nrm = sqrt(alpha * alpha + sigma);
@@ -592,30 +605,34 @@ __global__ void __launch_bounds__(32) sym_lmax_kernel(const double* __restrict__
     const double tau = (beta - alpha) / beta;
     const double scal = 1.0 / (alpha - beta);
     const double vi = (lane == k + 1) ? 1.0 : ((lane > k + 1 && lane < b) ? A[lane][k] * scal : 0.0);
-    vs[lane] = vi;
-    if (lane == 0) e[k] = beta;
-    __syncwarp();
-    // p = tau A22 v ; w = p - (tau/2)(p'v) v ; A22 -= v w' + w v'
-    double pi = 0.0;
-    if (lane > k && lane < b)
-      for (int j = k + 1; j < b; ++j) pi = fma(A[lane][j], vs[j], pi);
-    pi *= tau;
+    // p = tau A22 v, one warp-reduced row at a time
+    for (int i = k + 1 + warp; i < b; i += NW) {
+      const double pr = warp_sum((lane > k && lane < b) ? A[i][lane] * vi : 0.0);
+      if (lane == 0) ps[i] = tau * pr;
+    }
+    __syncthreads();
+    const double pi = (lane > k && lane < b) ? ps[lane] : 0.0;
+    // w = p - (tau/2)(p'v) v ; A22 -= v w' + w v'
     const double kk = -0.5 * tau * warp_sum(pi * vi);
     const double wi = fma(kk, vi, pi);
-    ws[lane] = wi;
-    __syncwarp();
-    if (lane > k && lane < b)
-      for (int j = k + 1; j < b; ++j) A[lane][j] -= vi * ws[j] + wi * vs[j];
-    __syncwarp();
+    if (tid == 0) {
+      d[k] = A[k][k];
+      e[k] = beta;
+    }
+    for (int i = k + 1 + warp; i < b; i += NW) {
+      const double vr = __shfl_sync(0xffffffffu, vi, i), wr = __shfl_sync(0xffffffffu, wi, i);
+      if (lane > k && lane < b) A[i][lane] -= vr * wi + wr * vi;
+    }
+    __syncthreads();
   }
-  if (lane == 0) {
+  if (tid == 0) {
     if (b >= 2) {
       d[b - 2] = A[b - 2][b - 2];
       e[b - 2] = A[b - 1][b - 2];
     }
     d[b - 1] = A[b - 1][b - 1];
   }
-  __syncwarp();
+  __syncthreads();
   // Gershgorin bracket of lambda_max
   double lo = 1e308, hi = -1e308, emax2 = 0.0;
   for (int i = 0; i < b; ++i) {
@@ -630,7 +647,7 @@ __global__ void __launch_bounds__(32) sym_lmax_kernel(const double* __restrict__
   hi += 4.0 * 2.220446049250313e-16 * span + pivmin;
   // multisection: count(x) = #eigenvalues < x; lambda_max in [lo, hi)
   for (int step = 0; step < 64; ++step) {
-    const double x = lo + (hi - lo) * ((double)(lane + 1) / 33.0);
+    const double x = lo + (hi - lo) * ((double)(tid + 1) / (double)(LMAX_THREADS + 1));
     int cnt = 0;
     double q = d[0] - x;
     if (fabs(q) < pivmin) q = -pivmin;
@@ -640,22 +657,27 @@ __global__ void __launch_bounds__(32) sym_lmax_kernel(const double* __restrict__
       if (fabs(q) < pivmin) q = -pivmin;
       cnt += (q < 0.0);
     }
-    // smallest shift above lambda_max (cnt == b)
+    xs[tid] = x;
+    // smallest shift above lambda_max (cnt == b); counts are monotone in x
     const unsigned above = __ballot_sync(0xffffffffu, cnt == b);
+    if (lane == 0) cs[warp] = above ? warp * 32 + __ffs(above) - 1 : LMAX_THREADS;
+    __syncthreads();
+    int f = LMAX_THREADS;
+    for (int w = 0; w < NW; ++w) f = min(f, cs[w]);
     double nlo = lo, nhi = hi;
-    if (above) {
-      const int f = __ffs(above) - 1;
-      nhi = __shfl_sync(0xffffffffu, x, f);
-      if (f > 0) nlo = __shfl_sync(0xffffffffu, x, f - 1);
+    if (f < LMAX_THREADS) {
+      nhi = xs[f];
+      if (f > 0) nlo = xs[f - 1];
     } else {
-      nlo = __shfl_sync(0xffffffffu, x, 31);
+      nlo = xs[LMAX_THREADS - 1];
     }
+    __syncthreads();
     if (nlo == lo && nhi == hi) break;
     lo = nlo;
     hi = nhi;
     if (hi - lo <= 2.220446049250313e-16 * fmax(fabs(lo), fabs(hi))) break;
   }
-  if (lane == 0) out[0] = 0.5 * (lo + hi);
+  if (tid == 0) out[0] = 0.5 * (lo + hi);
 }
 
 }  // namespace small
