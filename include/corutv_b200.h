@@ -52,6 +52,8 @@ typedef int (*corutv_allreduce_fn)(void* user, double* buf, int64_t count, void*
  * (a cudaStream_t, or NULL for the legacy default stream). */
 int corutv_create(int device, void* stream, corutv_handle** out);
 void corutv_destroy(corutv_handle* h);
+/* Rebind the handle to `stream`; the new stream is ordered after the work
+ * already queued on the old one (it still reads the handle's workspace). */
 int corutv_set_stream(corutv_handle* h, void* stream);
 const char* corutv_last_error(const corutv_handle* h);
 int corutv_version(void);
@@ -60,6 +62,12 @@ int corutv_version(void);
  * matrix; sketches over the column space are combined with `fn`
  * (SURVEY §8e).  world == 1 (or fn == NULL) restores single-GPU mode. */
 int corutv_set_comm(corutv_handle* h, corutv_allreduce_fn fn, void* user, int rank, int world);
+
+/* Row-sharded mode: the global row count of the matrices of the following
+ * calls (the same on every rank), so no call needs a row-count collective
+ * and host sync.  0 = unknown (one allreduce per call).  Reset by
+ * corutv_set_comm. */
+int corutv_set_global_rows(corutv_handle* h, int64_t m_global);
 
 /* CoR-UTV: replaces corutv(a, cfg, counter) — sketch.py:182-208, including
  * _power_sketch (sketch.py:166-179), householder_qr of both sketches
@@ -88,10 +96,14 @@ int corutv_decompose_seeded(corutv_handle* h, const double* a, int64_t m, int64_
                             double* t, double* v, int64_t* perm, int64_t* passes_host);
 
 /* CoR-UTV truncated for the ALM thresholding step (rpca.py:122-132,
- * _truncate_utv): r = #(|diag T| > delta) is returned in *r_host and the QRCP
- * stops at step r (|diag T| is non-increasing), so only U[:, :r], T[:r, :]
- * (rows >= r zeroed), V and perm are formed.  Omega from `omega` (n x ell,
- * device) or, if NULL, drawn from pcg_state as corutv_decompose_seeded. */
+ * _truncate_utv): r = #(|diag T| > delta) is returned in *r_host.  The QRCP
+ * stops once the largest remaining (downdated) column norm is below delta
+ * (with a 1e-3 margin for the downdate error), so every diagonal entry that
+ * can exceed delta is computed and counted, as the reference counts the
+ * whole diagonal even where it is slightly non-monotone; U[:, :r], T's rows
+ * up to the last step taken (later rows zeroed), V and perm are formed.
+ * Omega from `omega` (n x ell, device) or, if NULL, drawn from pcg_state as
+ * corutv_decompose_seeded.  Any ell <= min(m, n). */
 int corutv_decompose_truncated(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda,
                                int ell, int q_power, int variant, const double* omega,
                                const uint64_t* pcg_state, double delta, double* u, double* t,
@@ -231,10 +243,17 @@ int corutv_lowrank_error_rank(corutv_handle* h, const double* a, int64_t m, int6
                               const double* u, const double* t, const double* v, int ell, int r,
                               double* out_host);
 
-/* Column-pivoted QR of a square n x n device matrix (dense.py:152-192,
- * Businger-Golub pivoting, first-index ties): q (n x n), r (n x n, upper),
- * perm (n) with a[:, perm] = q r.  n <= 640.  The harness's deterministic
- * "qrcp" method (bench.py:151-152, 208-211). */
+/* Column-pivoted QR of an m x n device matrix (qrcp, dense.py:152-192:
+ * Businger-Golub pivoting on downdated column norms with exact refresh,
+ * first-index ties): q (m x k, ld ldq), r (k x n upper, ld ldr), perm (n)
+ * with a[:, perm] = q r, k = min(m, n).  Square cores up to 640 run in one
+ * CTA or a thread-block cluster; anything else in one cooperative grid
+ * launch with the matrix in L2 (m + n/2 up to ~28000). */
+int corutv_qrcp_mn(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, double* q,
+                   int64_t ldq, double* r, int64_t ldr, int64_t* perm);
+
+/* Square case of corutv_qrcp_mn (q, r n x n, ld n): the harness's
+ * deterministic "qrcp" method (bench.py:151-152, 208-211). */
 int corutv_qrcp(corutv_handle* h, const double* a, int64_t n, int64_t lda, double* q, double* r,
                 int64_t* perm);
 
@@ -252,7 +271,20 @@ int corutv_spectral_norm(corutv_handle* h, const double* a, int64_t m, int64_t n
 int corutv_singular_values(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda,
                            double* sig);
 
-/* sum of squares of an m x n matrix (rpca.py:187, dense.py:94-96). */
+/* Number of non-finite entries of an m x n matrix (as_matrix's check,
+ * dense.py:48-49), this rank only; *count_host receives it. */
+int corutv_count_nonfinite(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda,
+                           int64_t* count_host);
+
+/* out = sign(x) max(|x| - delta, 0), elementwise (shrink, rpca.py:99-104);
+ * CORUTV_ERR_NONFINITE if x holds a non-finite entry (as_matrix,
+ * dense.py:48-49).  x, out: m x n device (ld ldx / ldo; out may be x). */
+int corutv_shrink(corutv_handle* h, const double* x, int64_t m, int64_t n, int64_t ldx, double delta,
+                  double* out, int64_t ldo);
+
+/* sum of squares of an m x n matrix (rpca.py:187, dense.py:94-96); in the
+ * row-sharded mode the sum over all ranks.  CORUTV_ERR_NONFINITE on every
+ * rank when any rank's block holds a non-finite entry. */
 int corutv_sumsq(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda,
                  double* out_host);
 

@@ -117,7 +117,19 @@ def ptr(t) -> int:
 
 
 def raise_if_nonfinite(t, name):
-    """Error-path only: reproduce as_matrix's finiteness message."""
-    torch = torch_mod()
-    if not bool(torch.isfinite(t).all()):
+    """as_matrix's finiteness check (dense.py:48-49) on the device
+    (corutv_count_nonfinite): ValueError "<name> contains non-finite
+    entries"."""
+    import ctypes
+
+    from . import _lib
+
+    if t.dim() != 2 or t.numel() == 0:
+        return
+    if t.stride(1) != 1 or t.stride(0) < t.shape[1] or str(t.dtype) != "torch.float64":
+        t = t.to(torch_mod().float64).contiguous()
+    cnt = ctypes.c_int64(0)
+    h = _lib.handle(t.device.index)
+    h.call("corutv_count_nonfinite", ptr(t), t.shape[0], t.shape[1], t.stride(0), ctypes.byref(cnt))
+    if cnt.value:
         raise ValueError(f"{name} contains non-finite entries")

@@ -54,6 +54,7 @@ SIGNATURES = {
     "corutv_jacobi_svd_warm": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _I64, _D, _I32, _VP, _VP, _VP]),
     "corutv_lowrank_error_rank": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _VP, _VP, _I32, _I32, c_double_p]),
     "corutv_qrcp": (_I32, [_VP, _VP, _I64, _I64, _VP, _VP, _VP]),
+    "corutv_qrcp_mn": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP]),
     "corutv_svt": (_I32, [_VP, _VP, _I64, _I64, _I64, _D, _I32, _VP, _I64, _VP, _VP, _VP, _VP,
                           ctypes.POINTER(_I32)]),
     "corutv_sor_svd": (_I32, [_VP, _VP, _I64, _I64, _I64, _I32, _I32, _I32, _VP, _VP, _VP, _VP, _VP,
@@ -71,6 +72,9 @@ SIGNATURES = {
                                     ctypes.POINTER(_I32)]),
     "corutv_singular_values": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP]),
     "corutv_sumsq": (_I32, [_VP, _VP, _I64, _I64, _I64, c_double_p]),
+    "corutv_count_nonfinite": (_I32, [_VP, _VP, _I64, _I64, _I64, c_int64_p]),
+    "corutv_shrink": (_I32, [_VP, _VP, _I64, _I64, _I64, _D, _VP, _I64]),
+    "corutv_set_global_rows": (_I32, [_VP, _I64]),
     "corutv_lowrank_error": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _VP, _VP, _I32, c_double_p]),
     "corutv_gemm": (_I32, [_VP, _I32, _I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _I64]),
     "corutv_profile_begin": (_I32, [_VP]),

@@ -73,23 +73,60 @@ __global__ void gather_cols_kernel(const double* __restrict__ Q, int64_t rows, i
 
 // per-block partial sums of squares (stage 1 of a deterministic reduction)
 __global__ void sumsq_partial_kernel(const double* __restrict__ A, int64_t rows, int64_t cols,
-                                     int64_t lda, double* __restrict__ part) {
+                                     int64_t lda, double* __restrict__ part, long long* __restrict__ bad) {
   __shared__ double red[32];
+  __shared__ int redb[32];
   double s = 0.0;
+  int nb = 0;  // non-finite entries seen (as_matrix's check, dense.py:48-49)
   const int64_t total = rows * cols;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = idx / cols, c = idx % cols;
     const double v = A[r * lda + c];
     s = fma(v, v, s);
+    nb += isfinite(v) ? 0 : 1;
   }
   s = warp_sum(s);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  nb = __reduce_add_sync(0xffffffffu, (unsigned)nb);
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = s;
+    redb[threadIdx.x >> 5] = nb;
+  }
   __syncthreads();
   if (threadIdx.x < 32) {
     s = (threadIdx.x < blockDim.x / 32) ? red[threadIdx.x] : 0.0;
+    nb = (threadIdx.x < blockDim.x / 32) ? redb[threadIdx.x] : 0;
     s = warp_sum(s);
-    if (threadIdx.x == 0) part[blockIdx.x] = s;
+    nb = __reduce_add_sync(0xffffffffu, (unsigned)nb);
+    if (threadIdx.x == 0) {
+      part[blockIdx.x] = s;
+      if (bad) bad[blockIdx.x] = nb;
+    }
+  }
+}
+
+// shrink (rpca.py:99-104): out = sign(x) max(|x| - delta, 0), counting
+// non-finite inputs into bad[blockIdx.x] (grid-stride, fixed partition)
+__global__ void shrink_kernel(const double* __restrict__ X, int64_t rows, int64_t cols, int64_t ldx,
+                              double delta, double* out, int64_t ldo, long long* __restrict__ bad) {
+  __shared__ int redb[32];
+  int nb = 0;
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / cols, c = idx % cols;
+    const double x = X[r * ldx + c];
+    nb += isfinite(x) ? 0 : 1;
+    const double sg = (x > 0.0) ? 1.0 : ((x < 0.0) ? -1.0 : x);  // np.sign
+    out[r * ldo + c] = sg * fmax(fabs(x) - delta, 0.0);
+  }
+  nb = __reduce_add_sync(0xffffffffu, (unsigned)nb);
+  if ((threadIdx.x & 31) == 0) redb[threadIdx.x >> 5] = nb;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    nb = (threadIdx.x < blockDim.x / 32) ? redb[threadIdx.x] : 0;
+    nb = __reduce_add_sync(0xffffffffu, (unsigned)nb);
+    if (threadIdx.x == 0) bad[blockIdx.x] = nb;
   }
 }
 
@@ -134,6 +171,22 @@ __global__ void snorm_init_kernel(double* vt, int b, int64_t n, int64_t ldv) {
     const int64_t i = idx % n;
     const int64_t count = (n - j + b - 1) / b;
     vt[j * ldv + i] = (i % b == j) ? 1.0 / sqrt((double)count) : 0.0;
+  }
+}
+
+// rows of the left factor scaled for the pseudoinverse (dense.py:390-402):
+// us[k][j] = ut[k][j] / sig_k when sig_k > max(len, nv) sig_0 1e-12, else 0
+// (the one-CTA Jacobi kernel's (W / s) / s, with ut = W / s).
+__global__ void pinv_scale_kernel(const double* __restrict__ ut, int64_t ldut, const double* __restrict__ sig,
+                                  int nv, int len, double* __restrict__ us, int64_t ldus) {
+  const double s0 = sig[0];
+  const double cut = (double)max(len, nv) * s0 * 1e-12;
+  const int64_t total = (int64_t)nv * len;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(idx / len), j = (int)(idx % len);
+    const double sk = sig[k];
+    us[k * ldus + j] = (s0 > 0.0 && sk > cut) ? ut[k * ldut + j] / sk : 0.0;
   }
 }
 

@@ -44,6 +44,11 @@ __device__ __forceinline__ unsigned long long gtime() {
 // the 4 rows a DMMA fragment touches fall on different bank halves)
 __host__ __device__ inline int stage_stride(int l) { return (l + 15) / 16 * 16 + 8; }
 __host__ __device__ inline int smem_doubles(int l) { return 2 * 32 * 33 + 32 * stage_stride(l); }
+// cores whose panel stage does not fit shared memory (l >~ 840) read the
+// panel straight from the L2-resident W instead (GSTAGE): after step (b)
+// the panel row kb + p, columns c0.., IS the stage row p (left block then
+// right half, contiguous), so only the pointer and the stride change
+__host__ __device__ inline int smem_doubles_gstage() { return 2 * 32 * 33; }
 
 // Warp-level Cholesky of the identity-padded 32 x 32 block in Ds (upper,
 // stride 33), in place, lane = column; Rinv[k] = 1 / R[k][k].  Returns the
@@ -92,12 +97,13 @@ __device__ bool factor_diag32(double* Ds, double* Rinv) {
 //      DMMA tiles (K = 32) spread over every warp of the cluster: the upper
 //      triangle of the left block and the nonzero band of the right half.
 // Two cluster barriers per panel.
+template <bool GSTAGE>
 __device__ bool chol_aug_cluster(cg::cluster_group& cluster, double* W, int l, double* smem, int* s_flag) {
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int rank = (int)cluster.block_rank(), CS = (int)cluster.num_blocks();
   const int nwarp = nt >> 5;
   const int ld = 2 * l;
-  const int wp = stage_stride(l);
+  const int wp = GSTAGE ? ld : stage_stride(l);
   double* Ds = smem;             // R_kk (upper), 32 x 33
   double* Rinv = smem + 32 * 33;  // 1 / diag(R_kk)
 
@@ -164,8 +170,10 @@ __device__ bool chol_aug_cluster(cg::cluster_group& cluster, double* W, int l, d
     if (c0 >= l) break;
     // (c) stage the panel (rows >= nb zero) with asynchronous 8-byte copies
     // (all of a thread's loads in flight at once), then update the trailing
-    // matrix
-    for (int e = tid; e < 32 * ncols; e += nt) {
+    // matrix.  GSTAGE: the panel rows in W are the stage (nb == 32 here:
+    // only the last panel is short, and it ends the loop above)
+    if (GSTAGE) stage = W + (int64_t)kb * ld + c0;
+    for (int e = tid; !GSTAGE && e < 32 * ncols; e += nt) {
       const int p = e / ncols, t = e % ncols;
       if (p < nb) {
         const int64_t col = (t < nleft) ? c0 + t : l + (t - nleft);
@@ -315,6 +323,7 @@ __device__ double cluster_sum(cg::cluster_group& cluster, double v, double* slot
   return s;
 }
 
+template <bool GSTAGE>
 __global__ void __launch_bounds__(THREADS, 1)
     chol_factor_cluster_kernel(const double* __restrict__ G, int l, int64_t ldg, double shift_coeff,
                                int allow_plain, double kappa_max, double* __restrict__ rinvT,
@@ -355,7 +364,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         W[(int64_t)i * ld + k] = g;
       }
       cluster.sync();
-      const bool fail = chol_aug_cluster(cluster, W, l, dsm, &s_flag);
+      const bool fail = chol_aug_cluster<GSTAGE>(cluster, W, l, dsm, &s_flag);
       cluster.sync();
       if (fail) {
         if (!shifted) { shifted = 1; continue; }

@@ -30,6 +30,7 @@
 #include "chol_cluster.cuh"
 #include "rng.cuh"
 #include "qrcp_cluster.cuh"
+#include "qrcp_grid.cuh"
 #include "small.cuh"
 #include "jacobi_grid.cuh"
 #include "skinny.cuh"
@@ -59,6 +60,9 @@ struct corutv_handle {
   unsigned char* tails = nullptr;
   int tails_cap = 0;
   cudaEvent_t est_ev = nullptr;  // spectral norm: readiness of the async estimate
+  cudaEvent_t switch_ev = nullptr;  // orders a new stream after the old one (set_stream)
+  int64_t m_global = 0;        // row-sharded mode: global rows stated by the host (0 = ask)
+  double* scal_dev = nullptr;  // device scalars for the fallback row-count allreduce
   // second compute stream: the two sketches' CholeskyQR steps run side by
   // side (a cluster Cholesky occupies 8-16 SMs; the other job's GEMMs fill
   // the rest)
@@ -510,16 +514,19 @@ void allreduce(corutv_handle* h, double* buf, int64_t count) {
 
 void sync(corutv_handle* h) { CK(cudaStreamSynchronize(h->stream)); }
 
+// Global row count of a row-sharded matrix.  The host layer normally states
+// it once per sharded call (corutv_set_global_rows): no collective, no sync.
+// Otherwise one 2-value allreduce; a rank with no rows is legal (its GEMMs
+// are empty and its partials zero), so no rank fails alone before a
+// collective the others are waiting in.
 double global_rows(corutv_handle* h, int64_t m_local) {
   if (h->world <= 1 || !h->ar_fn) return (double)m_local;
+  if (h->m_global > 0) return (double)h->m_global;
+  if (!h->scal_dev) CK(cudaMalloc(&h->scal_dev, 8 * sizeof(double)));
   h->pinned[0] = (double)m_local;
-  // route through a device scalar so the callback sees device memory
-  double* d;
-  CK(cudaMallocAsync(&d, sizeof(double), h->stream));
-  CK(cudaMemcpyAsync(d, h->pinned, sizeof(double), cudaMemcpyHostToDevice, h->stream));
-  allreduce(h, d, 1);
-  CK(cudaMemcpyAsync(h->pinned, d, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaFreeAsync(d, h->stream));
+  CK(cudaMemcpyAsync(h->scal_dev, h->pinned, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  allreduce(h, h->scal_dev, 1);
+  CK(cudaMemcpyAsync(h->pinned, h->scal_dev, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   sync(h);
   return h->pinned[0];
 }
@@ -572,14 +579,17 @@ void cholqr_multi(corutv_handle* h, QrJob* jobs, int njobs, int ell, int64_t ldx
   // updates) wins from l ~ 64 on (C2 l = 50: equal, C3 l = 110: -0.8 ms/step)
   static const bool force_cluster = std::getenv("CORUTV_CHOL_CLUSTER") != nullptr;  // tuning knob
   const bool smem = aug + static_smem <= (size_t)optin && l < 64 && !force_cluster;
-  const size_t cl_smem = (size_t)chc::smem_doubles(l) * 8;
+  // the cluster kernel stages each 32-row panel in shared memory up to
+  // l ~ 840; larger cores read the panel from L2 (GSTAGE)
+  const bool gstage = (size_t)chc::smem_doubles(l) * 8 > (size_t)optin;
+  const size_t cl_smem = (size_t)(gstage ? chc::smem_doubles_gstage() : chc::smem_doubles(l)) * 8;
+  auto cl_kern = gstage ? chc::chol_factor_cluster_kernel<true> : chc::chol_factor_cluster_kernel<false>;
   const int cl_cs = l >= 256 ? 16 : 8;
   if (smem) {
     set_smem(h, small::chol_factor_kernel, aug);
   } else {
-    set_smem(h, chc::chol_factor_cluster_kernel, cl_smem);
-    if (cl_cs > 8)
-      CK(cudaFuncSetAttribute(chc::chol_factor_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    set_smem(h, cl_kern, cl_smem);
+    if (cl_cs > 8) CK(cudaFuncSetAttribute(cl_kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   }
   auto launch_factor = [&](QrJob& q, double coeff) {
     if (smem) {
@@ -600,8 +610,8 @@ void cholqr_multi(corutv_handle* h, QrJob* jobs, int njobs, int ell, int64_t ldx
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, chc::chol_factor_cluster_kernel, (const double*)q.w.G, l, ldx, coeff, 1,
-                          kKappaPlain, q.w.rinvT, ldx, q.w.gwork, q.w.info));
+    CK(cudaLaunchKernelEx(&cfg, cl_kern, (const double*)q.w.G, l, ldx, coeff, 1, kKappaPlain, q.w.rinvT, ldx,
+                          q.w.gwork, q.w.info));
     ++h->launches;
   };
   auto run_step = [&](QrJob& q, int j) {
@@ -676,8 +686,57 @@ double* cholqr(corutv_handle* h, double* xa, double* xb, int64_t rows, int ell, 
 }
 
 // --------------------------------------------------------------- QRCP
-// l <= 32: one CTA (qrcp_kernel).  Larger cores: the thread-block-cluster
+// Grid QRCP (qrcp_grid.cuh) of an m x n row-major matrix: T (k x n, ld ldt),
+// qtT (k x m, ld ldq; row c = column c of Q), perm; k = min(m, n).
+void qrcp_grid(corutv_handle* h, const double* A, int m, int n, int64_t lda, double* T, int64_t ldt,
+               double* qtT, int64_t ldq, long long* perm_out, int* perm32, double delta, int* r_dev) {
+  const int k = std::min(m, n);
+  const size_t smem = qg::smem_bytes(m, n);
+  if (smem > (size_t)max_optin_smem(h))
+    fail(h, CORUTV_ERR_ARG, "qrcp: matrix too large for the grid kernel (m + n/2 above ~28000)");
+  set_smem(h, qg::qrcp_grid_kernel, smem);
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qg::qrcp_grid_kernel, qg::THREADS, smem));
+  if (per_sm < 1) fail(h, CORUTV_ERR_CUDA, "qrcp: grid kernel cannot be resident");
+  // one owned column per warp where possible; never more CTAs than SMs
+  // (each grid barrier costs more with every CTA)
+  const int G = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)h->num_sms,
+                                                             ((int64_t)n + qg::NW - 1) / qg::NW));
+  Arena ar(h);
+  qg::Params P{};
+  ar.add(&P.R, (size_t)m * n);
+  ar.add(&P.nrm, (size_t)n);
+  ar.add(&P.ref, (size_t)n);
+  ar.add(&P.done, (size_t)n);
+  ar.add(&P.cand_v, (size_t)2 * G);
+  ar.add(&P.cand_q, (size_t)2 * G);
+  ar.add(&P.diag, (size_t)k);
+  ar.add(&P.tau, (size_t)k);
+  ar.add(&P.vhead, (size_t)k);
+  ar.add(&P.has_ref, (size_t)k);
+  ar.commit();
+  P.a = A;
+  P.lda = lda;
+  P.m = m;
+  P.n = n;
+  P.k = k;
+  P.T = T;
+  P.ldt = ldt;
+  P.qtT = qtT;
+  P.ldq = ldq;
+  P.perm_out = perm_out;
+  P.perm32 = perm32;
+  P.delta = delta;
+  P.r_out = r_dev;
+  void* args[] = {&P};
+  CK(cudaLaunchCooperativeKernel((const void*)qg::qrcp_grid_kernel, dim3(G), dim3(qg::THREADS), args, smem,
+                                 h->stream));
+  ++h->launches;
+}
+
+// l <= 128: one CTA (qrcp_kernel).  Cores up to 640: the thread-block-cluster
 // kernel (qrcp_cluster.cuh) with the core spread over CS CTAs' shared memory.
+// Larger: the cooperative grid kernel with the core in L2 (qrcp_grid.cuh).
 void qrcp(corutv_handle* h, const double* D, int l, int64_t ldd, double* T, int64_t ldt, double* qtT,
           int64_t ldq, long long* perm_out, int* perm32, double* gwork, double delta = -1.0,
           int* r_dev = nullptr) {
@@ -700,6 +759,10 @@ void qrcp(corutv_handle* h, const double* D, int l, int64_t ldd, double* T, int6
     CK_LAUNCH();
     return;
   }
+  if (l > qc::LMAX) {
+    qrcp_grid(h, D, l, l, ldd, T, ldt, qtT, ldq, perm_out, perm32, delta, r_dev);
+    return;
+  }
   // cluster size: enough CTAs that R (and Q when possible) fit on chip
   const size_t stat = sizeof(qc::Shared) + 1024;
   int cs = 2;
@@ -714,8 +777,10 @@ void qrcp(corutv_handle* h, const double* D, int l, int64_t ldd, double* T, int6
   }
   const int cw = (l + cs - 1) / cs;
   const size_t dyn = (size_t)cw * l * 8 * (q_smem ? 2 : 1);
-  if (cw > qc::MAXCW || dyn + stat > (size_t)optin)
-    fail(h, CORUTV_ERR_ARG, "QRCP core too large for a 16-CTA cluster");
+  if (cw > qc::MAXCW || dyn + stat > (size_t)optin) {
+    qrcp_grid(h, D, l, l, ldd, T, ldt, qtT, ldq, perm_out, perm32, delta, r_dev);
+    return;
+  }
   set_smem(h, qc::qrcp_cluster_kernel, dyn);
   if (cs > 8) CK(cudaFuncSetAttribute(qc::qrcp_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
@@ -796,7 +861,25 @@ void jacobi(corutv_handle* h, const double* X, int nv, int len, int64_t ldx, dou
     jacobi_grid(h, X, nv, len, ldx, sig, status, ut, ldut, vt, ldvt, tol, max_sweeps);
     return;
   }
-  if (nv > small::LMAX) fail(h, CORUTV_ERR_ARG, "pseudoinverse core above the supported maximum 640");
+  if (nv > small::LMAX) {
+    // pinv of a core beyond one CTA: the grid SVD, then pinv = V S^+ U^T as
+    // one DMMA GEMM over the cutoff-scaled left factor
+    const int64_t ldu = round_up(len, 16), ldv = round_up(nv, 16);
+    Arena ar(h);
+    double *ut, *vt, *us, *ws;
+    ar.add(&ut, (size_t)nv * ldu);
+    ar.add(&us, (size_t)nv * ldu);
+    ar.add(&vt, (size_t)nv * ldv);
+    ar.add(&ws, gemm_ws_elems(h, nv, len, nv) + 16);
+    ar.commit();
+    jacobi_grid(h, X, nv, len, ldx, sig, status, ut, ldu, vt, ldv, tol, max_sweeps);
+    int nb, tb;
+    launch_grid_1d((int64_t)nv * len, &nb, &tb);
+    aux::pinv_scale_kernel<<<nb, tb, 0, h->stream>>>(ut, ldu, sig, nv, len, us, ldu);
+    CK_LAUNCH();
+    run_gemm(h, true, nv, len, nv, vt, ldv, us, ldu, pinv, ldp, nullptr, 0, ws);
+    return;
+  }
   if (smem) {
     set_smem(h, small::jacobi_kernel<true>, bytes);
     small::jacobi_kernel<true><<<1, jt, bytes, h->stream>>>(X, nv, len, ldx, tol, max_sweeps, sig, pinv, ldp, ut, ldut,
@@ -1079,14 +1162,16 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
                int64_t* perm, int64_t* passes_host, double delta = -1.0, int* r_host = nullptr,
                const HostFeed* feed = nullptr, double* svd_sigma = nullptr) {
   if (!a || (!omega && !pcg) || !u || (!t && !svd_sigma) || !v) fail(h, CORUTV_ERR_ARG, "null pointer argument");
-  if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
+  const bool sharded = h->world > 1 && h->ar_fn;
+  // a rank of a row-sharded matrix may own no rows; the global shape is
+  // checked below, identically on every rank
+  if ((sharded ? m < 0 : m < 1) || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
   if (ell < 1) fail(h, CORUTV_ERR_ARG, "ell must be >= 1, got " + std::to_string(ell));
-  if (ell > small::LMAX) fail(h, CORUTV_ERR_ARG, "ell above the supported maximum 640");
   if (q < 0) fail(h, CORUTV_ERR_ARG, "q_power must be >= 0");
   if (variant != CORUTV_EXACT_D && variant != CORUTV_APPROX_D) fail(h, CORUTV_ERR_ARG, "bad variant");
   if (lda < n) fail(h, CORUTV_ERR_ARG, "lda < n");
-  const bool sharded = h->world > 1 && h->ar_fn;
   const double mg = global_rows(h, m);
+  if (mg < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
   if (mg < (double)n)
     fail(h, CORUTV_ERR_SHAPE, "corutv requires rows >= cols, got " + std::to_string((long long)mg) + "x" + std::to_string(n));
   if ((double)ell > std::min(mg, (double)n))
@@ -1303,7 +1388,6 @@ void tsr(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, i
   if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
   if (h->world > 1 && h->ar_fn) fail(h, CORUTV_ERR_ARG, "tsr_svd: row-sharded mode is not supported");
   if (ell < 1) fail(h, CORUTV_ERR_ARG, "ell must be >= 1, got " + std::to_string(ell));
-  if (ell > small::LMAX) fail(h, CORUTV_ERR_ARG, "ell above the supported maximum 640");
   if ((int64_t)ell > std::min(m, n))
     fail(h, CORUTV_ERR_SHAPE, "ell=" + std::to_string(ell) + " exceeds min(m, n)=" + std::to_string(std::min(m, n)));
   if (lda < n) fail(h, CORUTV_ERR_ARG, "lda < n");
@@ -1483,6 +1567,12 @@ void lowrank_op(corutv_handle* h, int mode, const double* u, const double* t, co
   CUtensorMap mw = make_map(h, Wt, std::max(r, 1), cols, ldr, 16 * J);
   p.part_sum = part;
   p.part_cnt = cnt;
+  // double2 epilogue accesses need an even ld and 16-byte aligned bases (a
+  // caller's view such as X[:, 1:] is only 8-byte aligned)
+  {
+    auto al = [](const void* q) { return q == nullptr || (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+    p.vec = ((p.ld & 1) == 0) && al(p.m_mat) && al(p.s) && al(p.y) && al(p.g_next);
+  }
   if (mode == gemm::LR_STORE) launch_lr<gemm::LR_STORE>(h, J, mu, mw, tl, p, grid);
   else if (mode == gemm::LR_ALM) launch_lr<gemm::LR_ALM>(h, J, mu, mw, tl, p, grid);
   else launch_lr<gemm::LR_RESID>(h, J, mu, mw, tl, p, grid);
@@ -1497,20 +1587,26 @@ void lowrank_op(corutv_handle* h, int mode, const double* u, const double* t, co
   }
 }
 
+// sum of squares (all ranks); a non-finite entry on ANY rank raises on
+// every rank (the count is all-reduced with the sum), so no rank is left
+// waiting in a later collective.
 double sumsq(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda) {
   const int blocks = 148 * 8;
   Arena ar(h);
   double *part, *out;
+  long long* bad;
   ar.add(&part, blocks);
+  ar.add(&bad, blocks);
   ar.add(&out, 2);
   ar.commit();
-  aux::sumsq_partial_kernel<<<blocks, 256, 0, h->stream>>>(a, m, n, lda, part);
+  aux::sumsq_partial_kernel<<<blocks, 256, 0, h->stream>>>(a, m, n, lda, part, bad);
   CK_LAUNCH();
-  aux::finalize_sums_kernel<<<1, 1024, 0, h->stream>>>(part, nullptr, blocks, out);
+  aux::finalize_sums_kernel<<<1, 1024, 0, h->stream>>>(part, bad, blocks, out);
   CK_LAUNCH();
   if (h->world > 1 && h->ar_fn) allreduce(h, out, 2);
-  CK(cudaMemcpyAsync(h->pinned, out, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(h->pinned, out, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   sync(h);
+  if (h->pinned[1] != 0.0) fail(h, CORUTV_ERR_NONFINITE, "matrix contains non-finite entries");
   return h->pinned[0];
 }
 
@@ -1761,6 +1857,8 @@ void corutv_destroy(corutv_handle* h) {
   if (h->staging) cudaFreeHost(h->staging);
   if (h->tails) cudaFreeHost(h->tails);
   if (h->est_ev) cudaEventDestroy(h->est_ev);
+  if (h->switch_ev) cudaEventDestroy(h->switch_ev);
+  if (h->scal_dev) cudaFree(h->scal_dev);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   if (h->side) {
     cudaStreamSynchronize(h->side);
@@ -1773,7 +1871,22 @@ void corutv_destroy(corutv_handle* h) {
 
 int corutv_set_stream(corutv_handle* hh, void* stream) {
   if (!hh) return CORUTV_ERR_ARG;
-  hh->stream = reinterpret_cast<cudaStream_t>(stream);
+  cudaStream_t ns = reinterpret_cast<cudaStream_t>(stream);
+  if (ns == hh->stream) return CORUTV_OK;
+  // work queued on the old stream (the U lift, the V gather, a speculative
+  // power step, the Gaussian tail patch) still reads the handle's arena and
+  // pinned scratch: the new stream must not reuse them before it finishes
+  cudaSetDevice(hh->device);
+  if (!hh->switch_ev && cudaEventCreateWithFlags(&hh->switch_ev, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    return CORUTV_ERR_CUDA;
+  }
+  if (cudaEventRecord(hh->switch_ev, hh->stream) != cudaSuccess ||
+      cudaStreamWaitEvent(ns, hh->switch_ev, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return CORUTV_ERR_CUDA;
+  }
+  hh->stream = ns;
   return CORUTV_OK;
 }
 
@@ -1785,6 +1898,13 @@ int corutv_set_comm(corutv_handle* h, corutv_allreduce_fn fn, void* user, int ra
   h->ar_user = user;
   h->rank = rank;
   h->world = world;
+  h->m_global = 0;
+  return CORUTV_OK;
+}
+
+int corutv_set_global_rows(corutv_handle* h, int64_t m_global) {
+  if (!h || m_global < 0) return CORUTV_ERR_ARG;
+  h->m_global = m_global;
   return CORUTV_OK;
 }
 
@@ -2224,25 +2344,33 @@ int corutv_lowrank_error_rank(corutv_handle* hh, const double* a, int64_t m, int
   ABI_END
 }
 
-int corutv_qrcp(corutv_handle* hh, const double* a, int64_t n, int64_t lda, double* q, double* r,
-                int64_t* perm) {
+int corutv_qrcp_mn(corutv_handle* hh, const double* a, int64_t m, int64_t n, int64_t lda, double* q,
+                   int64_t ldq, double* r, int64_t ldr, int64_t* perm) {
   ABI_BEGIN(hh)
   if (!a || !q || !r || !perm) fail(h, CORUTV_ERR_ARG, "null pointer argument");
-  if (n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
-  if (n > small::LMAX) fail(h, CORUTV_ERR_ARG, "qrcp: n above the supported maximum 640");
-  if (lda < n) fail(h, CORUTV_ERR_ARG, "lda < n");
-  const int l = (int)n;
-  const int64_t ldp = round_up(l, 16);
+  if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
+  const int64_t k = std::min(m, n);
+  if (lda < n || ldq < k || ldr < n) fail(h, CORUTV_ERR_ARG, "leading dimension too small");
+  if (m > (1 << 30) || n > (1 << 30)) fail(h, CORUTV_ERR_ARG, "qrcp: dimension too large");
+  const int64_t ldp = round_up(std::max(m, n), 16);
   Arena ar(h);
   double *qtT, *gwork;
   int* perm32;
-  ar.add(&qtT, (size_t)l * ldp);
-  ar.add(&gwork, (size_t)(l + 2) * (2 * l + 4) + 2 * (size_t)l * l + 16);
-  ar.add(&perm32, (size_t)ldp);
+  ar.add(&qtT, (size_t)k * ldp);
+  ar.add(&perm32, (size_t)n);
+  const bool core = m == n && n <= small::LMAX;
+  if (core) ar.add(&gwork, (size_t)(n + 2) * (2 * n + 4) + 2 * (size_t)n * n + 16);
   ar.commit();
-  qrcp(h, a, l, lda, r, l, qtT, ldp, reinterpret_cast<long long*>(perm), perm32, gwork);
-  transpose(h, qtT, l, l, ldp, q, l);  // Q = qtT'
+  if (core) qrcp(h, a, (int)n, lda, r, ldr, qtT, ldp, reinterpret_cast<long long*>(perm), perm32, gwork);
+  else qrcp_grid(h, a, (int)m, (int)n, lda, r, ldr, qtT, ldp, reinterpret_cast<long long*>(perm), perm32, -1.0,
+                 nullptr);
+  transpose(h, qtT, k, m, ldp, q, ldq);  // Q = qtT'
   ABI_END
+}
+
+int corutv_qrcp(corutv_handle* hh, const double* a, int64_t n, int64_t lda, double* q, double* r,
+                int64_t* perm) {
+  return corutv_qrcp_mn(hh, a, n, n, lda, q, n, r, n, perm);
 }
 
 int corutv_spectral_norm(corutv_handle* hh, const double* a, int64_t m, int64_t n, int64_t lda, double tol,
@@ -2260,6 +2388,53 @@ int corutv_singular_values(corutv_handle* hh, const double* a, int64_t m, int64_
                            double* sig) {
   ABI_BEGIN(hh)
   singular_values(h, a, m, n, lda, sig);
+  ABI_END
+}
+
+int corutv_count_nonfinite(corutv_handle* hh, const double* a, int64_t m, int64_t n, int64_t lda,
+                           int64_t* count_host) {
+  ABI_BEGIN(hh)
+  if (!a || m < 0 || n < 0 || lda < n) fail(h, CORUTV_ERR_ARG, "bad matrix arguments");
+  const int blocks = 148 * 8;
+  Arena ar(h);
+  double *part, *out;
+  long long* bad;
+  ar.add(&part, blocks);
+  ar.add(&bad, blocks);
+  ar.add(&out, 2);
+  ar.commit();
+  aux::sumsq_partial_kernel<<<blocks, 256, 0, h->stream>>>(a, m, n, lda, part, bad);
+  CK_LAUNCH();
+  aux::finalize_sums_kernel<<<1, 1024, 0, h->stream>>>(part, bad, blocks, out);
+  CK_LAUNCH();
+  CK(cudaMemcpyAsync(h->pinned, out + 1, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  sync(h);
+  if (count_host) *count_host = (int64_t)llround(h->pinned[0]);
+  ABI_END
+}
+
+int corutv_shrink(corutv_handle* hh, const double* x, int64_t m, int64_t n, int64_t ldx, double delta,
+                  double* out, int64_t ldo) {
+  ABI_BEGIN(hh)
+  if (!x || !out || m < 0 || n < 0 || ldx < n || ldo < n) fail(h, CORUTV_ERR_ARG, "bad matrix arguments");
+  if (!(delta >= 0.0)) fail(h, CORUTV_ERR_ARG, "delta must be >= 0");
+  int blocks, tb;
+  launch_grid_1d(m * n, &blocks, &tb);
+  Arena ar(h);
+  double *o2, *zero;
+  long long* bad;
+  ar.add(&bad, blocks);
+  ar.add(&zero, blocks);
+  ar.add(&o2, 2);
+  ar.commit();
+  CK(cudaMemsetAsync(zero, 0, sizeof(double) * blocks, h->stream));
+  aux::shrink_kernel<<<blocks, tb, 0, h->stream>>>(x, m, n, ldx, delta, out, ldo, bad);
+  CK_LAUNCH();
+  aux::finalize_sums_kernel<<<1, 1024, 0, h->stream>>>(zero, bad, blocks, o2);
+  CK_LAUNCH();
+  CK(cudaMemcpyAsync(h->pinned, o2 + 1, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  sync(h);
+  if (h->pinned[0] != 0.0) fail(h, CORUTV_ERR_NONFINITE, "x contains non-finite entries");
   ABI_END
 }
 

@@ -351,6 +351,8 @@ struct LrParams {
   double mu, lam_over_mu, mu_next;
   double* part_sum;      // per-CTA partial sum of squares
   long long* part_cnt;   // per-CTA partial nnz
+  int vec;               // 16-byte (double2) accesses allowed: ld even and every
+                         // n x n operand 16-byte aligned (checked on the host)
 };
 
 template <int J, int MODE>
@@ -411,7 +413,7 @@ __global__ void __launch_bounds__(THREADS, 2)
   double ssum = 0.0;
   long long cnt = 0;
   const int ncols = min(TN, t.N - n0);
-  const bool vec = ((p.ld & 1) == 0);
+  const bool vec = p.vec != 0;
   // Each warp owns rows {4w .. 4w+3} + 32k; a batch of RB rows has all its
   // M / Y loads issued before any store (Y is read and written, so loads
   // of later rows could not otherwise move above earlier stores), keeping

@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   cluster.sync();
 
   int kend = l;
+  int rcount = 0;  // #(|diag T| > delta) over the steps taken (rpca.py:123-124)
   for (int j = 0; j < l; ++j) {
     const int par = j & 1;
     const int* cur = sh.l2p[par];
@@ -117,6 +118,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int q = sh.cand_q[par][r];
       if (v > best || (v == best && q < bq)) { best = v; bq = q; }
     }
+    // truncation: stop once no remaining column can give |diag T| > delta
+    // (small.cuh qrcp_body; identical in every CTA)
+    if (delta >= 0.0 && best * 1.001 < delta * delta) {
+      kend = j;
+      break;
+    }
     const int p = bq;
     const int pc = cur[p];
     const int owner = pc / cw;
@@ -136,10 +143,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const double v0 = refl ? x0 + (x0 >= 0.0 ? nx : -nx) : 0.0;
     const double tj = refl ? 2.0 / (v0 * v0 + t2) : 0.0;
     const double dj = refl ? x0 - v0 * (tj * (v0 * x0 + t2)) : x0;
-    if (delta >= 0.0 && !(fabs(dj) > delta)) {  // identical in every CTA
-      kend = j;
-      break;
-    }
+    rcount += (fabs(dj) > delta) ? 1 : 0;
     if (threadIdx.x == 0) {
       sh.diag[j] = dj;
       sh.tau[j] = tj;
@@ -192,7 +196,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (perm_out) perm_out[c] = fin[c];
       perm32[c] = fin[c];
     }
-    if (threadIdx.x == 0 && r_out) *r_out = kend;
+    if (threadIdx.x == 0 && r_out) *r_out = delta >= 0.0 ? rcount : kend;
   }
 
   // explicit Q: this CTA's Q columns [c_lo, c_lo + nown)

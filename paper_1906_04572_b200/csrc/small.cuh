@@ -199,12 +199,13 @@ __device__ __forceinline__ double group_sum(double v) {
 template <int G, int LM>
 __device__ int qrcp_body(double* R, double* Q, int l, double* nrm, double* ref, double* tau,
                          double* vhead, double* diag, int (*l2p)[LM], int* done, int* has_ref,
-                         const int** fin_out, double delta) {
+                         const int** fin_out, double delta, int* rcount_out) {
   const int lane = threadIdx.x & 31;
   const int nt = blockDim.x;
   const int gid = threadIdx.x / G, gl = threadIdx.x % G;
   const int ngroups = nt / G;
   int kend = l;
+  int rcount = 0;  // #(|diag T| > delta) over the steps taken (rpca.py:123-124)
   for (int j = 0; j < l; ++j) {
     const int* cur = l2p[j & 1];
     int* nxt = l2p[(j + 1) & 1];
@@ -221,6 +222,15 @@ __device__ int qrcp_body(double* R, double* Q, int l, double* nrm, double* ref, 
       const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
       if (ov > best || (ov == best && oq < bq)) { best = ov; bq = oq; }
     }
+    // truncation (delta >= 0): stop once no remaining column can give
+    // |diag T| > delta -- the largest downdated norm^2 (within 1e-3 of the
+    // true one: refreshed below 1e-10 of its reference) is below delta^2.
+    // The reference counts the whole diagonal (rpca.py:123-124), which may
+    // be slightly non-monotone around delta; steps up to here are counted
+    if (delta >= 0.0 && best * 1.001 < delta * delta) {
+      kend = j;
+      break;
+    }
     const int p = bq;
     const int pc = cur[p];
     // reflector of x = R[j:, pc] (dense.py:104-114), every warp
@@ -233,11 +243,7 @@ __device__ int qrcp_body(double* R, double* Q, int l, double* nrm, double* ref, 
     const double v0 = refl ? x0 + (x0 >= 0.0 ? nx : -nx) : 0.0;
     const double tj = refl ? 2.0 / (v0 * v0 + t2) : 0.0;
     const double dj = refl ? x0 - v0 * (tj * (v0 * x0 + t2)) : x0;
-    if (delta >= 0.0 && !(fabs(dj) > delta)) {
-      // |diag T| is non-increasing: r = j (rpca.py:123-124); stop here
-      kend = j;
-      break;
-    }
+    rcount += (fabs(dj) > delta) ? 1 : 0;
     for (int q = threadIdx.x; q < l; q += nt) nxt[q] = (q == j) ? cur[p] : ((q == p) ? cur[j] : cur[q]);
     if (threadIdx.x == 0) {
       diag[j] = dj;
@@ -285,6 +291,7 @@ __device__ int qrcp_body(double* R, double* Q, int l, double* nrm, double* ref, 
   __syncthreads();
   const int* fin = l2p[kend & 1];
   *fin_out = fin;
+  *rcount_out = delta >= 0.0 ? rcount : kend;
 
   // explicit Q by reverse accumulation on the identity (dense.py:117-129)
   for (int i = threadIdx.x >> 5; i < l; i += nt >> 5)
@@ -359,14 +366,15 @@ __global__ void __launch_bounds__(1024, 1)
   }
   __syncthreads();
   const int* fin = nullptr;
-  const int kend = qrcp_body<G, LM>(R, Q, l, nrm, ref, tau, vhead, diag, l2p, done, has_ref, &fin, delta);
+  int rcount = 0;
+  const int kend = qrcp_body<G, LM>(R, Q, l, nrm, ref, tau, vhead, diag, l2p, done, has_ref, &fin, delta, &rcount);
   __syncthreads();
   for (int i = threadIdx.x >> 5; i < l; i += nt >> 5)
     for (int c = lane; c < l; c += 32) {
       T[i * ldt + c] = (i >= kend) ? 0.0 : ((c > i) ? R[i * l + fin[c]] : ((c == i) ? diag[i] : 0.0));
       qtT[c * ldq + i] = Q[i * l + c];
     }
-  if (threadIdx.x == 0 && r_out) *r_out = kend;
+  if (threadIdx.x == 0 && r_out) *r_out = rcount;
   for (int c = threadIdx.x; c < l; c += nt) {
     if (perm_out) perm_out[c] = fin[c];
     perm32[c] = fin[c];

@@ -6,6 +6,8 @@
 * :func:`frobenius_norm` — dense.py:94-96
 * :func:`jacobi_svd` — dense.py:313-376 (sor_svd / tsr_svd cores, the
   InexactALM baseline's warm-started SVT)
+* :func:`qrcp` — dense.py:152-192 (the QRCP of the compressed core, and the
+  harness's deterministic full-matrix method)
 """
 
 from __future__ import annotations
@@ -18,7 +20,7 @@ from . import _device as dev
 from . import _lib
 
 __all__ = ["spectral_norm", "singular_values", "frobenius_norm", "spectral_norm_iters", "SvdFactors",
-           "jacobi_svd", "JACOBI_TOL", "JACOBI_MAX_SWEEPS"]
+           "QrcpFactors", "qrcp", "jacobi_svd", "JACOBI_TOL", "JACOBI_MAX_SWEEPS"]
 
 JACOBI_TOL = 1e-14        # dense.py:34
 JACOBI_MAX_SWEEPS = 100   # dense.py:36
@@ -77,9 +79,10 @@ def frobenius_norm(a) -> float:
     A, _ = dev.to_device(a, "a")
     out = ctypes.c_double(0.0)
     h = _lib.handle(A.device.index)
-    h.call("corutv_sumsq", dev.ptr(A), A.shape[0], A.shape[1], A.stride(0), ctypes.byref(out))
-    if not math.isfinite(out.value):
-        dev.raise_if_nonfinite(A, "a")
+    try:
+        h.call("corutv_sumsq", dev.ptr(A), A.shape[0], A.shape[1], A.stride(0), ctypes.byref(out))
+    except ValueError:
+        raise ValueError("a contains non-finite entries") from None
     return math.sqrt(out.value)
 
 
@@ -91,6 +94,34 @@ def _check_v_init(v_init, k: int):
     if tuple(V.shape) != (k, k):
         raise ValueError(f"v_init must be {k}x{k}, got {tuple(V.shape)}")
     return V
+
+
+@dataclass
+class QrcpFactors:
+    """dense.py:62-69: ``q @ r == a[:, perm]`` with ``|diag(r)|``
+    non-increasing."""
+
+    q: object
+    r: object
+    perm: object
+
+
+def qrcp(a) -> QrcpFactors:
+    """dense.py:152-192 on the device (corutv_qrcp_mn): Businger-Golub
+    column pivoting on downdated norms with exact refresh, ties to the lowest
+    column index; q is m x k, r is k x n, k = min(m, n)."""
+    torch = dev.torch_mod()
+    A, was_host = dev.to_device(a, "a")
+    dev.raise_if_nonfinite(A, "a")
+    m, n = A.shape
+    k = min(m, n)
+    q = torch.empty((m, k), dtype=torch.float64, device=A.device)
+    r = torch.empty((k, n), dtype=torch.float64, device=A.device)
+    perm = torch.empty((n,), dtype=torch.int64, device=A.device)
+    h = _lib.handle(A.device.index)
+    h.call("corutv_qrcp_mn", dev.ptr(A), m, n, A.stride(0), dev.ptr(q), k, dev.ptr(r), n, dev.ptr(perm))
+    return QrcpFactors(q=dev.to_output(q, was_host), r=dev.to_output(r, was_host),
+                       perm=dev.to_output(perm, was_host))
 
 
 def jacobi_svd(a, tol: float = JACOBI_TOL, max_sweeps: int = JACOBI_MAX_SWEEPS,

@@ -82,9 +82,23 @@ class RowShardComm:
         except Exception:  # pragma: no cover - surfaced as CORUTV_ERR_COMM
             return 1
 
-    def attach(self, handle: "_lib.Handle") -> None:
+    def global_rows(self, m_local: int) -> int:
+        """Sum of the ranks' row counts (one host collective per sharded
+        call; the library then needs no row-count exchange of its own)."""
+        import torch
+        import torch.distributed as tdist
+
+        dev_ = "cuda" if self.device == "cuda" else "cpu"
+        t = torch.tensor([float(m_local)], dtype=torch.float64, device=dev_)
+        tdist.all_reduce(t, op=tdist.ReduceOp.SUM, group=self.group)
+        return int(t.item())
+
+    def attach(self, handle: "_lib.Handle", global_rows: int | None = None) -> None:
         _lib.check(handle.lib.corutv_set_comm(handle.ptr, self.callback, None, self.rank, self.world),
                    handle.ptr, "corutv_set_comm")
+        if global_rows is not None:
+            _lib.check(handle.lib.corutv_set_global_rows(handle.ptr, int(global_rows)), handle.ptr,
+                       "corutv_set_global_rows")
 
     def detach(self, handle: "_lib.Handle") -> None:
         handle.lib.corutv_set_comm(handle.ptr, _lib.ALLREDUCE_FN(), None, 0, 1)
@@ -109,7 +123,7 @@ def corutv_sharded(a_local, cfg: SketchConfig, comm: RowShardComm, counter: Pass
     perm = torch.empty((ell,), dtype=torch.int64, device=A.device)
     passes = ctypes.c_int64(0)
     h = _lib.handle(A.device.index)
-    comm.attach(h)
+    comm.attach(h, comm.global_rows(m_loc))
     try:
         if om is None:  # every rank draws the identical Omega on its device
             h.call("corutv_decompose_seeded", dev.ptr(A), m_loc, n, A.stride(0), ell, cfg.q_power,
@@ -144,7 +158,7 @@ def alm_corutv_sharded(m_local, cfg, comm: RowShardComm, global_rows: int):
     torch = dev.torch_mod()
     device = m_local.device.index if dev.is_device_tensor(m_local) else torch.cuda.current_device()
     h = _lib.handle(device)
-    comm.attach(h)
+    comm.attach(h, global_rows)
     try:
         def step(g, delta, cap, j, state):
             scfg = SketchConfig(ell=cap, q_power=cfg.q_power, seed=(cfg.seed + j) % 2 ** 64)

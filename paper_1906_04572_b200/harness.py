@@ -37,7 +37,7 @@ from . import _lib
 from .dense import singular_values
 from .errors import CorutvError
 from .rpca import AlmConfig, alm_corutv, inexact_alm, write_telemetry_csv
-from .sketch import VARIANT_EXACT, SketchConfig, corutv, flop_estimate, sor_svd, tsr_svd
+from .sketch import VARIANT_EXACT, SketchConfig, corutv, flop_estimate, sor_svd, svd_flop_estimate, tsr_svd
 from .synth import NoisyLowRankSpec, RpcaInstanceSpec, gen_noisy_lowrank, gen_rpca_instance
 
 __all__ = [
@@ -167,13 +167,6 @@ def write_csv(path, header: str, rows) -> None:
         fh.write(header + "\n")
         for row in rows:
             fh.write(",".join(_fmt(x) for x in row) + "\n")
-
-
-def svd_flop_estimate(m: int, n: int) -> int:
-    """sketch.py:299-304."""
-    if m < n:
-        m, n = n, m
-    return 14 * m * n ** 2 + 8 * n ** 3
 
 
 # ------------------------------------------------------------ device methods

@@ -89,8 +89,11 @@ def shrink(x, delta: float):
         raise ValueError("delta must be >= 0")
     torch = dev.torch_mod()
     t, was_host = dev.to_device(x, "x")
-    dev.raise_if_nonfinite(t, "x")
-    out = torch.sign(t) * torch.clamp_min(t.abs() - delta, 0.0)
+    out = torch.empty(tuple(t.shape), dtype=torch.float64, device=t.device)
+    h = _lib.handle(t.device.index)
+    # one fused pass: the finiteness check of as_matrix and the shrinkage
+    h.call("corutv_shrink", dev.ptr(t), t.shape[0], t.shape[1], t.stride(0), float(delta), dev.ptr(out),
+           out.stride(0))
     return dev.to_output(out, was_host)
 
 
@@ -192,9 +195,11 @@ def _alm_loop(m, cfg: AlmConfig, step, cap0, global_rows: int | None = None) -> 
     handle = _lib.handle(M.device.index)
     lam = cfg.lam if cfg.lam is not None else 1.0 / np.sqrt(max(hg, w_))
     ss = ctypes.c_double(0.0)
-    handle.call("corutv_sumsq", dev.ptr(M), h_, w_, M.stride(0), ctypes.byref(ss))
-    if not math.isfinite(ss.value):
-        dev.raise_if_nonfinite(M, "m")
+    try:
+        # the non-finite count is all-reduced with the sum: every rank raises
+        handle.call("corutv_sumsq", dev.ptr(M), h_, w_, M.stride(0), ctypes.byref(ss))
+    except ValueError:
+        raise ValueError("m contains non-finite entries") from None
     norm_m = float(np.sqrt(ss.value))
     if norm_m == 0.0:
         zero = torch.zeros_like(M)

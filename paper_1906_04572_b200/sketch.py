@@ -33,6 +33,7 @@ __all__ = [
     "corutv_lowrank_error",
     "count_passes",
     "flop_estimate",
+    "svd_flop_estimate",
     "sor_svd",
     "tsr_svd",
     "SvdFactors",
@@ -434,3 +435,10 @@ def flop_estimate(m: int, n: int, ell: int, q_power: int = 0, variant: str = VAR
     total += (8 * ell ** 3) // 3
     total += 2 * m * ell ** 2 + 2 * n * ell
     return total
+
+
+def svd_flop_estimate(m: int, n: int) -> int:
+    """sketch.py:299-304: textbook flop count of a full economy SVD."""
+    if m < n:
+        m, n = n, m
+    return 14 * m * n ** 2 + 8 * n ** 3
