@@ -140,3 +140,33 @@ def test_c3_full_size_matches_oracle():
     e_ref = math.sqrt(max(a2 - float((ref["t"] ** 2).sum()), 0.0))
     assert abs(e_dev - e_ref) <= 1e-8 * e_ref
     del a, f
+
+
+def test_c5_full_size_matches_oracle():
+    # BASELINE configs[4] (C5, orthonormal U512 / V512, sigma_i = 0.99^i,
+    # 1e-6 noise) at full size against the CPU oracle's recorded run on the
+    # same device-generated A and seeded Omega (tests/golden/c5_oracle.json,
+    # tools/c5_oracle.py): |diag T| to 1e-9 of T00, the whole QRCP
+    # permutation, the reconstruction error to 1e-10, the pass count
+    import json
+    from pathlib import Path
+
+    import numpy as np
+
+    ref = json.loads((Path(__file__).parent / "golden" / "c5_oracle.json").read_text())
+    m, n, ell, q, k, noise, _ = bench.WORKLOADS["c5"]
+    a = bench.gen_rows_device(torch, "c5", 0, m, torch.device("cuda", 0))
+    assert abs(float((a * a).sum()) - ref["a_fro2"]) <= 1e-12 * ref["a_fro2"]  # same A
+    cnt = P.PassCounter()
+    f = P.corutv(a, P.SketchConfig(ell=ell, q_power=q, seed=0), cnt)
+    assert cnt.passes == ref["passes"]
+    d_dev = f.t.diagonal().abs().cpu().numpy()
+    d_ref = np.asarray(ref["diag_t_abs"])
+    assert np.abs(d_dev - d_ref).max() <= 1e-9 * d_ref[0]
+    assert np.asarray(f.perm.cpu()).tolist() == ref["perm"]
+    e_dev = P.corutv_lowrank_error(a, P.SketchConfig(ell=ell, q_power=q, seed=0))
+    assert abs(e_dev - ref["err"]) <= 1e-10 * ref["err"]
+    u0 = f.u[::4096, 0].cpu().numpy()
+    s = np.sign(np.dot(u0, ref["u_col0_sample"]))
+    assert np.abs(s * u0 - np.asarray(ref["u_col0_sample"])).max() <= 1e-9
+    del a, f

@@ -75,10 +75,13 @@ def test_corutv_ell1000_matches_oracle(decaying, variant):
 
 def test_corutv_ell1000_c2_distribution():
     """BASELINE configs[1]'s matrix (sigma = 1 for i <= 40, then 0.8^(i-40))
-    at ell = 1000, q = 1: past i ~ 200 the spectrum is below rounding, so the
-    trailing sketch directions are noise for the oracle and the device
-    alike; both errors sit at the rounding floor and the determined part of
-    |diag T| (and the pivots of the 40 unit singular directions) agree."""
+    at ell = 1000, q = 1.  C1 = (A A') A Omega carries direction i only while
+    sigma_i^3 > u sigma_1^3, i.e. sigma_i > ~5e-6 (i <~ 95): beyond that the
+    sketch is rounding noise for the oracle and the device alike, so both
+    errors sit at that floor (~2e-5 |A|, measured 1.8e-5 oracle / 2.4e-5
+    device) and only the captured part of |diag T| is determined -- to
+    1e-9 of T00 where sigma_i^3 > 1e9 u (i <= 60) -- with the pivots of the
+    40 unit singular directions."""
     rng = np.random.Generator(np.random.PCG64(11))
     m, n = 4000, 3000
     u = np.linalg.qr(rng.standard_normal((m, n)))[0]
@@ -92,9 +95,10 @@ def test_corutv_ell1000_c2_distribution():
     na = np.linalg.norm(a)
     e_ref = O.corutv_lowrank_error(a, ref)
     e_dev = np.linalg.norm(a - f.lowrank())
-    assert e_ref <= 1e-12 * na and e_dev <= 1e-12 * na, (e_ref / na, e_dev / na)
+    assert e_ref <= 1e-4 * na and e_dev <= 1e-4 * na, (e_ref / na, e_dev / na)
+    assert 0.5 <= e_dev / e_ref <= 2.0, (e_ref / na, e_dev / na)
     dref = np.abs(np.diag(ref["t"]))
-    lead = 120  # sigma_120 = 0.8^80 ~ 2e-8: well above the noise
+    lead = 60
     assert np.abs(np.abs(np.diag(f.t))[:lead] - dref[:lead]).max() <= 1e-9 * dref[0]
     assert np.array_equal(f.perm[:40], ref["perm"][:40])
     assert np.abs(f.u.T @ f.u - np.eye(ell)).max() < 1e-10
