@@ -63,6 +63,22 @@ int corutv_version(void);
  * (SURVEY §8e).  world == 1 (or fn == NULL) restores single-GPU mode. */
 int corutv_set_comm(corutv_handle* h, corutv_allreduce_fn fn, void* user, int rank, int world);
 
+/* Native NCCL data plane of the row-sharded mode: every
+ * exchange point (the n x ell sketch sum, the Gram of the row-sharded Q1
+ * sketch, the ell x ell core, the spectral norm's Gram and n x b block, the
+ * ALM scalars) is an ncclAllReduce enqueued by the library on the handle's
+ * stream -- no host callback, no host synchronisation of its own.
+ *   corutv_nccl_unique_id : rank 0 creates the 128-byte ncclUniqueId (the
+ *                           host layer broadcasts it, e.g. over its store);
+ *   corutv_nccl_init      : every rank joins (ncclCommInitRank); the handle
+ *                           owns the communicator;
+ *   corutv_set_nccl       : attach a caller-owned ncclComm_t (NULL detaches).
+ * NCCL (libnccl.so.2) is resolved at run time.  A one-rank communicator
+ * runs the sharded code path on one GPU.  corutv_set_comm detaches it. */
+int corutv_nccl_unique_id(unsigned char* id_out);
+int corutv_nccl_init(corutv_handle* h, const unsigned char* id, int rank, int world);
+int corutv_set_nccl(corutv_handle* h, void* nccl_comm, int rank, int world);
+
 /* Row-sharded mode: the global row count of the matrices of the following
  * calls (the same on every rank), so no call needs a row-count collective
  * and host sync.  0 = unknown (one allreduce per call).  Reset by

@@ -9,6 +9,8 @@
 
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -34,6 +36,7 @@
 #include "small.cuh"
 #include "jacobi_grid.cuh"
 #include "skinny.cuh"
+#include "snorm.cuh"
 
 #define CORUTV_VERSION 100
 
@@ -62,6 +65,8 @@ struct corutv_handle {
   cudaEvent_t est_ev = nullptr;  // spectral norm: readiness of the async estimate
   cudaEvent_t switch_ev = nullptr;  // orders a new stream after the old one (set_stream)
   int64_t m_global = 0;        // row-sharded mode: global rows stated by the host (0 = ask)
+  ncclComm_t nccl = nullptr;   // native data plane (corutv_nccl_init / corutv_set_nccl)
+  bool nccl_owned = false;
   double* scal_dev = nullptr;  // device scalars for the fallback row-count allreduce
   // second compute stream: the two sketches' CholeskyQR steps run side by
   // side (a cluster Cholesky occupies 8-16 SMs; the other job's GEMMs fill
@@ -394,9 +399,12 @@ size_t gemm_ws_elems(const corutv_handle* h, int64_t M, int64_t N, int64_t K) {
 // C (M x N, ldc) and/or Ct (N x M, ldct).  ws: split-K partial scratch.
 // force: use this plan's split-K partition (a row block of a larger GEMM
 // then gets bit-identical rows).
+// partials != nullptr: leave the split-K partials in ws (splits slices of
+// stride M ldw, ld ldw = round_up(N, 2); one slice when not split) for a
+// fused consumer, skip the finalize, and return the plan in *partials.
 void run_gemm(corutv_handle* h, bool mm, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
           const double* B, int64_t ldb, double* C, int64_t ldc, double* Ct, int64_t ldct, double* ws,
-          int* bad_flag = nullptr, const GemmPlan* force = nullptr) {
+          int* bad_flag = nullptr, const GemmPlan* force = nullptr, GemmPlan* partials = nullptr) {
   if (M <= 0 || N <= 0) return;
   int tb, nb;
   if (K <= 0) {
@@ -432,12 +440,18 @@ void run_gemm(corutv_handle* h, bool mm, int64_t M, int64_t N, int64_t K, const 
     if ((bn % 16 == 0 || p.n_tiles == 1) && make_map3d(h, B, N, K, ldb, gemm::nb16_of(p.J, p.WN), &mb)) t.mm3d |= 2;
     else mb = make_map(h, B, N, K, ldb, gemm::BK);
   }
+  // opt-in: stream A evict-first when it is read once (one column tile) and
+  // much larger than L2 (measured: C3 sweeps unchanged, the spectral norm's
+  // N = 24 sweeps 4 % slower, and its split-K partials still missed L2)
+  static const bool l2_hint = std::getenv("CORUTV_L2_HINT") != nullptr;
+  if (l2_hint && p.n_tiles == 1 && (double)M * (double)K * 8.0 > 256.0 * (1 << 20)) t.mm3d |= 4;
   static const bool debug_plan = std::getenv("CORUTV_DEBUG_PLAN") != nullptr;
   if (debug_plan)
     std::fprintf(stderr, "[corutv] gemm %s M=%lld N=%lld K=%lld J=%d WN=%d tiles=%dx%d splits=%d kps=%d mm3d=%d\n",
                  mm ? "MM" : "KK", (long long)M, (long long)N, (long long)K, p.J, p.WN, p.m_tiles, p.n_tiles, p.splits,
                  p.kps, t.mm3d);
-  const bool direct = (p.splits == 1 && Ct == nullptr && C != nullptr);
+  if (partials) *partials = p;
+  const bool direct = !partials && (p.splits == 1 && Ct == nullptr && C != nullptr);
   const int64_t ldw = round_up(N, 2);
   gemm::StoreParams sp;
   sp.bad_flag = bad_flag;
@@ -458,7 +472,7 @@ void run_gemm(corutv_handle* h, bool mm, int64_t M, int64_t N, int64_t K, const 
     if (bad_flag) launch_gemm_j<false, true>(h, p.J, p.WN, ma, mb, t, sp, grid);
     else launch_gemm_j<false, false>(h, p.J, p.WN, ma, mb, t, sp, grid);
   }
-  if (!direct) {
+  if (!direct && !partials) {
     launch_grid_1d(M * N, &nb, &tb);
     aux::splitk_finalize_kernel<<<nb, tb, 0, h->stream>>>(ws, p.splits, M * ldw, M, N, ldw, C, ldc, Ct, ldct);
     CK_LAUNCH();
@@ -506,7 +520,58 @@ void copy2d(corutv_handle* h, const double* src, int64_t rows, int64_t cols, int
   CK_LAUNCH();
 }
 
+// NCCL, resolved at run time (libnccl.so.2 -- the copy torch already
+// loaded, if any): the library needs no link-time NCCL dependency
+struct NcclApi {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+const NcclApi& nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) return;
+    api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(lib, "ncclGetUniqueId"));
+    api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(lib, "ncclCommInitRank"));
+    api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(lib, "ncclAllReduce"));
+    api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(lib, "ncclCommDestroy"));
+    api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(lib, "ncclGetErrorString"));
+    api.ok = api.get_unique_id && api.comm_init_rank && api.all_reduce && api.comm_destroy && api.error_string;
+  });
+  return api;
+}
+
+void release_nccl(corutv_handle* h) {
+  if (h->nccl && h->nccl_owned) {
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    nccl_api().comm_destroy(h->nccl);
+  }
+  h->nccl = nullptr;
+  h->nccl_owned = false;
+}
+
+// row-sharded mode: a native NCCL communicator (any size) or a host
+// allreduce callback with world > 1
+inline bool is_sharded(const corutv_handle* h) { return h->nccl != nullptr || (h->world > 1 && h->ar_fn); }
+
+// Sum-allreduce in place at one of the algorithm's exchange points: NCCL
+// enqueued on the handle's stream (no host involvement), else the host
+// callback (the gloo test path).
 void allreduce(corutv_handle* h, double* buf, int64_t count) {
+  if (h->nccl) {
+    const NcclApi& api = nccl_api();
+    const ncclResult_t r = api.all_reduce(buf, buf, (size_t)count, ncclDouble, ncclSum, h->nccl, h->stream);
+    if (r != ncclSuccess) fail(h, CORUTV_ERR_COMM, std::string("ncclAllReduce: ") + api.error_string(r));
+    return;
+  }
   if (h->world <= 1 || !h->ar_fn) return;
   if (h->ar_fn(h->ar_user, buf, count, (void*)h->stream) != 0)
     fail(h, CORUTV_ERR_COMM, "allreduce callback failed");
@@ -520,7 +585,7 @@ void sync(corutv_handle* h) { CK(cudaStreamSynchronize(h->stream)); }
 // are empty and its partials zero), so no rank fails alone before a
 // collective the others are waiting in.
 double global_rows(corutv_handle* h, int64_t m_local) {
-  if (h->world <= 1 || !h->ar_fn) return (double)m_local;
+  if (!is_sharded(h)) return (double)m_local;
   if (h->m_global > 0) return (double)h->m_global;
   if (!h->scal_dev) CK(cudaMalloc(&h->scal_dev, 8 * sizeof(double)));
   h->pinned[0] = (double)m_local;
@@ -625,7 +690,10 @@ void cholqr_multi(corutv_handle* h, QrJob* jobs, int njobs, int ell, int64_t ldx
   };
   // two independent unsharded jobs with their own split-K scratch: job 1 on
   // the side stream, job 0 on the caller's (same kernels, same results)
-  const bool pair = njobs == 2 && jobs[0].w.ws != jobs[1].w.ws && !jobs[0].sharded && !jobs[1].sharded;
+  // (a sharded job's Gram allreduce may only run on the handle's stream: with
+  // NCCL it is enqueued there, so job 0 -- the row-sharded Q1 sketch -- can
+  // still pair with the replicated job 1 on the side stream)
+  const bool pair = njobs == 2 && jobs[0].w.ws != jobs[1].w.ws && (!jobs[0].sharded || h->nccl) && !jobs[1].sharded;
   if (pair && !h->side) {
     CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming));
@@ -1162,7 +1230,7 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
                int64_t* perm, int64_t* passes_host, double delta = -1.0, int* r_host = nullptr,
                const HostFeed* feed = nullptr, double* svd_sigma = nullptr) {
   if (!a || (!omega && !pcg) || !u || (!t && !svd_sigma) || !v) fail(h, CORUTV_ERR_ARG, "null pointer argument");
-  const bool sharded = h->world > 1 && h->ar_fn;
+  const bool sharded = is_sharded(h);
   // a rank of a row-sharded matrix may own no rows; the global shape is
   // checked below, identically on every rank
   if ((sharded ? m < 0 : m < 1) || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
@@ -1218,7 +1286,7 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   ar.add(&ws, wse + 16);
   // split-K scratch of the C2 sketch's CholeskyQR (runs beside the C1 one)
   double* ws_qr2 = nullptr;
-  if (!sharded) ar.add(&ws_qr2, std::max(gemm_ws_elems(h, l, l, n), gemm_ws_elems(h, n, l, l)) + 16);
+  if (!sharded || h->nccl) ar.add(&ws_qr2, std::max(gemm_ws_elems(h, l, l, n), gemm_ws_elems(h, n, l, l)) + 16);
   // host input: the first A' C1 sweep runs split by split as row chunks land
   const GemmPlan k2plan = plan_gemm(h, n, l, m, true);
   double* ws2 = nullptr;
@@ -1386,7 +1454,7 @@ void tsr(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, i
   if (!a || !u || !sigma || !v || (!psi && !pcg_psi) || (!phi && !pcg_phi))
     fail(h, CORUTV_ERR_ARG, "null pointer argument");
   if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
-  if (h->world > 1 && h->ar_fn) fail(h, CORUTV_ERR_ARG, "tsr_svd: row-sharded mode is not supported");
+  if (is_sharded(h)) fail(h, CORUTV_ERR_ARG, "tsr_svd: row-sharded mode is not supported");
   if (ell < 1) fail(h, CORUTV_ERR_ARG, "ell must be >= 1, got " + std::to_string(ell));
   if ((int64_t)ell > std::min(m, n))
     fail(h, CORUTV_ERR_SHAPE, "ell=" + std::to_string(ell) + " exceeds min(m, n)=" + std::to_string(std::min(m, n)));
@@ -1579,7 +1647,7 @@ void lowrank_op(corutv_handle* h, int mode, const double* u, const double* t, co
   if (mode != gemm::LR_STORE) {
     aux::finalize_sums_kernel<<<1, 1024, 0, h->stream>>>(part, mode == gemm::LR_ALM ? cnt : nullptr, grid, out);
     CK_LAUNCH();
-    if (h->world > 1 && h->ar_fn) allreduce(h, out, 2);
+    if (is_sharded(h)) allreduce(h, out, 2);
     CK(cudaMemcpyAsync(h->pinned, out, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     sync(h);
     out2[0] = h->pinned[0];
@@ -1603,7 +1671,7 @@ double sumsq(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t ld
   CK_LAUNCH();
   aux::finalize_sums_kernel<<<1, 1024, 0, h->stream>>>(part, bad, blocks, out);
   CK_LAUNCH();
-  if (h->world > 1 && h->ar_fn) allreduce(h, out, 2);
+  if (is_sharded(h)) allreduce(h, out, 2);
   CK(cudaMemcpyAsync(h->pinned, out, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   sync(h);
   if (h->pinned[1] != 0.0) fail(h, CORUTV_ERR_NONFINITE, "matrix contains non-finite entries");
@@ -1638,10 +1706,139 @@ void singular_values(corutv_handle* h, const double* a, int64_t m, int64_t n, in
 }
 
 // |A|_2, dense.py:405-442.
+struct SnormFallback {};  // the fused CholeskyQR needed more steps than launched
+
+void spectral_norm_legacy(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, double tol,
+                          int max_iter, double* out, int* iters);
+
+// Single-GPU block power iteration with the fused latency kernels of
+// snorm.cuh: per iteration two DMMA sweeps (their split-K partials left in
+// the workspace) and 2 + kApply small launches; one host sync per
+// iteration on the estimate (queued ahead of the next sweeps).
+void spectral_norm_fused(corutv_handle* h, const double* A, int64_t ldA, int64_t m, int64_t n, bool tall, int b,
+                         double tol, int max_iter, double* out, int* iters) {
+  constexpr int kApply = 2;
+  const int64_t np = tall ? n : m, mp = tall ? m : n;
+  const int64_t ldb2 = round_up(b, 16), ldnp = round_up(np, 16), ldmp = round_up(mp, 16);
+  const int64_t ldw = round_up(b, 2);
+  auto ctas = [&](int64_t rows) { return (int)std::max<int64_t>(1, std::min<int64_t>(h->num_sms, (rows + 31) / 32)); };
+  const int gw = ctas(mp), gz = ctas(np);
+  Arena ar(h);
+  double *vT, *v, *w, *wT = nullptr, *ws, *gpart, *gpart2, *lam;
+  sn::QrState* qst;
+  sn::WState* wst;
+  ar.add(&vT, (size_t)b * ldnp);
+  ar.add(&v, (size_t)np * ldb2);
+  ar.add(&w, (size_t)mp * ldb2);
+  if (!tall) ar.add(&wT, (size_t)b * ldmp);
+  ar.add(&ws, std::max(gemm_ws_elems(h, m, b, n), gemm_ws_elems(h, n, b, m)) + 16);
+  ar.add(&gpart, (size_t)std::max(gw, gz) * sn::B * sn::B);
+  ar.add(&gpart2, (size_t)sn::GS * sn::B * sn::B);
+  ar.add(&lam, 2);
+  double* gram_w;
+  ar.add(&gram_w, (size_t)sn::B * sn::B);
+  ar.add((char**)&qst, sizeof(sn::QrState));
+  ar.add((char**)&wst, sizeof(sn::WState));
+  ar.commit();
+  CK(cudaMemsetAsync(qst, 0, sizeof(sn::QrState), h->stream));
+  CK(cudaMemsetAsync(wst, 0, sizeof(sn::WState), h->stream));
+  int nb, tb;
+  launch_grid_1d(b * np, &nb, &tb);
+  aux::snorm_init_kernel<<<nb, tb, 0, h->stream>>>(vT, b, np, ldnp);
+  CK_LAUNCH();
+  transpose(h, vT, b, np, ldnp, v, ldb2);
+  const double coeff = 11.0 * ((double)np * b + (double)b * (b + 1)) * kUnit;
+  int* st_pinned = reinterpret_cast<int*>(h->pinned + 16);
+  // lambda_max (the estimate) runs on the side stream, overlapped with the
+  // z = A' w sweep; only the host's stop test waits for it
+  if (!h->side) {
+    CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->join_ev, cudaEventDisableTiming));
+  }
+  double prev = 0.0;
+  for (int it = 0; it < max_iter; ++it) {
+    GemmPlan pw, pz;
+    // w = A' v  (A' = A if tall else A^T), partials -> w (+ w^T), lambda_max(w'w)
+    if (tall) run_gemm(h, false, m, b, n, A, ldA, vT, ldnp, nullptr, 0, nullptr, 0, ws, nullptr, nullptr, &pw);
+    else run_gemm(h, true, n, b, m, A, ldA, v, ldb2, nullptr, 0, nullptr, 0, ws, nullptr, nullptr, &pw);
+    if (it > 0) CK(cudaStreamWaitEvent(h->stream, h->est_ev, 0));  // gram_w is free again
+    sn::finalize_kernel<0><<<gw, sn::THREADS, 0, h->stream>>>(ws, pw.splits, mp * ldw, ldw, mp, b, w, ldb2, wT, ldmp,
+                                                             gpart, gpart2, wst->tickets, gram_w, qst, 0.0, 0.0,
+                                                             it > 0 ? 1 : 0);
+    CK_LAUNCH();
+    CK(cudaEventRecord(h->fork_ev, h->stream));
+    CK(cudaStreamWaitEvent(h->side, h->fork_ev, 0));
+    sn::lmax_kernel<<<1, sn::THREADS, 0, h->side>>>(gram_w, sn::B, b, lam);
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(h->pinned + 8, lam, sizeof(double), cudaMemcpyDeviceToHost, h->side));
+    CK(cudaEventRecord(h->est_ev, h->side));
+    // z = A'^T w, partials -> v, CholeskyQR in place
+    if (tall) run_gemm(h, true, n, b, m, A, ldA, w, ldb2, nullptr, 0, nullptr, 0, ws, nullptr, nullptr, &pz);
+    else run_gemm(h, false, m, b, n, A, ldA, wT, ldmp, nullptr, 0, nullptr, 0, ws, nullptr, nullptr, &pz);
+    sn::finalize_kernel<1><<<gz, sn::THREADS, 0, h->stream>>>(ws, pz.splits, np * ldw, ldw, np, b, v, ldb2, vT, ldnp,
+                                                             gpart, gpart2, qst->tickets, nullptr, qst, coeff,
+                                                             kKappaPlain, 0);
+    CK_LAUNCH();
+    // typically: apply R1 + factor 2 (final: the next finalize applies it), no-op
+    for (int s = 0; s < kApply; ++s) {
+      sn::apply_kernel<<<gz, sn::THREADS, 0, h->stream>>>(v, ldb2, vT, ldnp, np, b, gpart, gpart2, qst, coeff,
+                                                          kKappaPlain, s == kApply - 1 ? 1 : 0);
+      CK_LAUNCH();
+    }
+    // status of this iteration's QR, read with the next estimate
+    CK(cudaMemcpyAsync(st_pinned + 2 * (it & 1), &qst->status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaEventSynchronize(h->est_ev));
+    if (it > 0) {
+      const int qs = st_pinned[2 * ((it - 1) & 1)];
+      if (qs == 2) fail(h, CORUTV_ERR_NONFINITE, "sketch contains non-finite entries");
+      if (qs == 3) throw SnormFallback{};
+    }
+    const double est = std::sqrt(std::max(h->pinned[8], 0.0));
+    static const bool dbg = std::getenv("CORUTV_SNORM_DEBUG") != nullptr;
+    if (dbg) std::fprintf(stderr, "[snorm fused] it %d est %.17g lam %.17g rel %.3e\n", it, est, h->pinned[8],
+                          prev > 0 ? std::fabs(est - prev) / est : 0.0);
+    if (iters) *iters = it + 1;
+    if (est == 0.0) { *out = 0.0; return; }
+    if (std::fabs(est - prev) <= 0.02 * tol * est) { *out = est; return; }
+    prev = est;
+  }
+  *out = prev;
+  fail(h, CORUTV_ERR_CONVERGENCE, "spectral norm power iteration did not converge");
+}
+
 void spectral_norm(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, double tol,
                    int max_iter, double* out, int* iters) {
+  static const bool legacy = std::getenv("CORUTV_SNORM_LEGACY") != nullptr;  // A/B knob
+  const bool sharded = is_sharded(h);
+  if (!legacy && !sharded && m >= 1 && n >= 1 && std::min(m, n) > 64) {
+    const bool tall = m >= n;
+    const int b = (int)std::min<int64_t>(24, tall ? n : m);
+    const bool a_ok = ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && (lda % 2 == 0);
+    try {
+      if (a_ok) {
+        spectral_norm_fused(h, a, lda, m, n, tall, b, tol, max_iter, out, iters);
+      } else {
+        Arena ar(h);
+        double* apad;
+        const int64_t ldA = round_up(n, 16);
+        ar.add(&apad, (size_t)m * ldA);
+        ar.commit();
+        copy2d(h, a, m, n, lda, apad, ldA);
+        spectral_norm_fused(h, apad, ldA, m, n, tall, b, tol, max_iter, out, iters);
+      }
+      return;
+    } catch (const SnormFallback&) {
+      sync(h);  // rare: an orthonormalisation needed more steps; redo robustly
+    }
+  }
+  spectral_norm_legacy(h, a, m, n, lda, tol, max_iter, out, iters);
+}
+
+void spectral_norm_legacy(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, double tol,
+                          int max_iter, double* out, int* iters) {
   if (m < 1 || n < 1) fail(h, CORUTV_ERR_SHAPE, "a must have positive dimensions");
-  const bool sharded = h->world > 1 && h->ar_fn;
+  const bool sharded = is_sharded(h);
   const double mg = global_rows(h, m);
   if (std::min(mg, (double)n) <= 64) {
     if (sharded) fail(h, CORUTV_ERR_ARG, "spectral_norm: the Jacobi path is single-GPU only");
@@ -1781,6 +1978,9 @@ void spectral_norm(corutv_handle* h, const double* a, int64_t m, int64_t n, int6
       transpose(h, v, np, b, ldb2, vT, ldnp);
     }
     const double est = std::sqrt(std::max(h->pinned[8], 0.0));
+    static const bool dbg = std::getenv("CORUTV_SNORM_DEBUG") != nullptr;
+    if (dbg) std::fprintf(stderr, "[snorm legacy] it %d est %.17g lam %.17g rel %.3e\n", it, est, h->pinned[8],
+                          prev > 0 ? std::fabs(est - prev) / est : 0.0);
     if (iters) *iters = it + 1;
     if (est == 0.0) { *out = 0.0; return; }
     if (std::fabs(est - prev) <= 0.02 * tol * est) { *out = est; return; }
@@ -1849,6 +2049,7 @@ int corutv_create(int device, void* stream, corutv_handle** out) {
 void corutv_destroy(corutv_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
+  release_nccl(h);
   if (h->stream) cudaStreamSynchronize(h->stream);
   else cudaDeviceSynchronize();
   if (h->arena) cudaFree(h->arena);
@@ -1894,12 +2095,58 @@ const char* corutv_last_error(const corutv_handle* h) { return h ? h->err.c_str(
 
 int corutv_set_comm(corutv_handle* h, corutv_allreduce_fn fn, void* user, int rank, int world) {
   if (!h || world < 1 || rank < 0 || rank >= world) return CORUTV_ERR_ARG;
+  release_nccl(h);
   h->ar_fn = fn;
   h->ar_user = user;
   h->rank = rank;
   h->world = world;
   h->m_global = 0;
   return CORUTV_OK;
+}
+
+int corutv_nccl_unique_id(unsigned char* id_out) {
+  if (!id_out) return CORUTV_ERR_ARG;
+  const NcclApi& api = nccl_api();
+  if (!api.ok) return CORUTV_ERR_COMM;
+  ncclUniqueId id;
+  if (api.get_unique_id(&id) != ncclSuccess) return CORUTV_ERR_COMM;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(id_out, &id, sizeof(id));
+  return CORUTV_OK;
+}
+
+int corutv_nccl_init(corutv_handle* hh, const unsigned char* id, int rank, int world) {
+  ABI_BEGIN(hh)
+  if (!id || world < 1 || rank < 0 || rank >= world) fail(h, CORUTV_ERR_ARG, "bad NCCL rank/world");
+  const NcclApi& api = nccl_api();
+  if (!api.ok) fail(h, CORUTV_ERR_COMM, "libnccl.so.2 not found");
+  release_nccl(h);
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  ncclComm_t comm = nullptr;
+  const ncclResult_t r = api.comm_init_rank(&comm, world, uid, rank);
+  if (r != ncclSuccess) fail(h, CORUTV_ERR_COMM, std::string("ncclCommInitRank: ") + api.error_string(r));
+  h->nccl = comm;
+  h->nccl_owned = true;
+  h->ar_fn = nullptr;
+  h->rank = rank;
+  h->world = world;
+  h->m_global = 0;
+  ABI_END
+}
+
+int corutv_set_nccl(corutv_handle* hh, void* comm, int rank, int world) {
+  ABI_BEGIN(hh)
+  if (world < 1 || rank < 0 || rank >= world) fail(h, CORUTV_ERR_ARG, "bad NCCL rank/world");
+  if (comm && !nccl_api().ok) fail(h, CORUTV_ERR_COMM, "libnccl.so.2 not found");
+  release_nccl(h);
+  h->nccl = reinterpret_cast<ncclComm_t>(comm);
+  h->nccl_owned = false;
+  h->ar_fn = nullptr;
+  h->rank = comm ? rank : 0;
+  h->world = comm ? world : 1;
+  h->m_global = 0;
+  ABI_END
 }
 
 int corutv_set_global_rows(corutv_handle* h, int64_t m_global) {

@@ -61,7 +61,8 @@ struct Tile {
   int k_tiles;          // total k tiles (ceil(K / 16))
   int k_tiles_per_split;
   int splits;
-  int mm3d;             // MM operands as one 3-D box per stage: bit 0 A, bit 1 B
+  int mm3d;             // MM operands as one 3-D box per stage: bit 0 A, bit 1 B;
+                        // bit 2: A (the data matrix, read once) loaded evict-first
 };
 
 // Accumulator for one consumer warp: 4 (M) x J (N) DMMA fragments.
@@ -106,19 +107,25 @@ __device__ __forceinline__ void issue_stage(const Smem& sm, const CUtensorMap* m
   mbar_arrive_expect_tx(&sm.full[st], stage_tx(J, WN, MM));
   double* sa = sm.a + st * (BMW * BK);
   double* sb = sm.b + st * (NB16 * 16 * BK);
+  const bool ef = (mm3d & 4) != 0;
+  const uint64_t pol = ef ? policy_evict_first() : 0;
   if (!MM) {
-    tma_load_2d(sa, mapA, &sm.full[st], kt * BK, m0);
+    if (ef) tma_load_2d_hint(sa, mapA, &sm.full[st], kt * BK, m0, pol);
+    else tma_load_2d(sa, mapA, &sm.full[st], kt * BK, m0);
     tma_load_2d(sb, mapB, &sm.full[st], kt * BK, n0);
   } else {
     // mm3d bit 0 / bit 1: A / B fetched as one 3-D box {16 cols, rows, column
     // groups} (lands as [group][row][16]); otherwise one 2-D box per 16
     // columns (B columns need not start on a 16-column group)
     if (mm3d & 1) {
-      tma_load_3d(sa, mapA, &sm.full[st], 0, kt * BK, m0 / 16);
+      if (ef) tma_load_3d_hint(sa, mapA, &sm.full[st], 0, kt * BK, m0 / 16, pol);
+      else tma_load_3d(sa, mapA, &sm.full[st], 0, kt * BK, m0 / 16);
     } else {
 #pragma unroll
-      for (int bx = 0; bx < BMW / 16; ++bx)
-        tma_load_2d(sa + bx * 16 * BK, mapA, &sm.full[st], m0 + 16 * bx, kt * BK);
+      for (int bx = 0; bx < BMW / 16; ++bx) {
+        if (ef) tma_load_2d_hint(sa + bx * 16 * BK, mapA, &sm.full[st], m0 + 16 * bx, kt * BK, pol);
+        else tma_load_2d(sa + bx * 16 * BK, mapA, &sm.full[st], m0 + 16 * bx, kt * BK);
+      }
     }
     if (mm3d & 2) {
       tma_load_3d(sb, mapB, &sm.full[st], 0, kt * BK, n0 / 16);

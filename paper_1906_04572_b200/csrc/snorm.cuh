@@ -35,133 +35,170 @@ struct QrState {
   int done;               // Q complete (apply launches return at once)
   int status;             // 0 ok, 2 non-finite, 3 not converged within the launched steps
   int steps;
-  unsigned ticket;        // last-CTA election (reset by the last CTA)
+  unsigned ticket;        // last-CTA election of a finishing apply (reset by it)
+  unsigned tickets[16];   // two-level Gram reduction: [0] final, [1 + g] group g
 };
 
 struct WState {
-  unsigned ticket;
+  unsigned tickets[16];
 };
 
-// Cholesky G + shift I = R'R of the b x b matrix in smem (ld ldg), padded to
-// 32 x 32 with the identity, lane c holding column c; then R^-1 (upper).
-// Returns false when a pivot is not positive/finite.  nr2 / ni2: |R|_F^2,
-// |R^-1|_F^2 (warp-uniform).
-__device__ bool warp_chol_inv(const double* Gs, int ldg, int b, double shift, double (&x)[B], double& nr2,
-                              double& ni2) {
-  const int lane = threadIdx.x & 31;
-  double a[B];
+constexpr int GS = 16;  // CTAs per first-level reduction group
+
+// The serial 32 x 32 algorithms below run in ONE warp of the last CTA, once
+// per launch: they keep the matrix in shared memory and use rolled loops, so
+// the code stays small (fully unrolled register versions measured ~100 us a
+// launch, dominated by instruction fetch of straight-line code run once).
+constexpr int LDW = B + 1;
+
+// CTA-wide Cholesky of the augmented [G + shift I | I] (32 x 64, identity-
+// padded past b): the row operations that turn the left half into R (R'R =
+// G + shift I) turn the right half into R^-T, so no separate triangular
+// inverse (small.cuh chol_aug_unblocked).  Register-blocked: thread t owns
+// row t/8, columns 8 (t%8) .. +7; per column j the pivot's owner publishes
+// W[j][j], row j's owners scale and publish row j, every row below takes
+// its rank-1 update -- two barriers per column.  Returns false (uniform) on
+// a non-positive or non-finite pivot; nr2 / ni2 = |R|_F^2, |R^-1|_F^2 of the
+// b x b block; on return the owners' registers are written to W (smem,
+// 32 x LDA).
+constexpr int LDA = 2 * B + 1;
+static_assert(THREADS == 256, "cta_chol_aug: 32 rows x 8 threads");
+
+__device__ bool cta_chol_aug(const double* Gs, int ldg, int b, double shift, double* W, double* red,
+                             double* rowj, double* piv, double& nr2, double& ni2) {
+  const int tid = threadIdx.x;
+  const int i = tid >> 3, cb = (tid & 7) * 8;
+  double w[8];
 #pragma unroll
-  for (int i = 0; i < B; ++i) {
-    double g = (i < b && lane < b) ? Gs[i * ldg + lane] : (i == lane ? 1.0 : 0.0);
-    if (i == lane && lane < b) g += shift;
-    a[i] = g;
+  for (int q = 0; q < 8; ++q) {
+    const int c = cb + q;
+    double g;
+    if (c < B) {
+      g = (i < b && c < b) ? Gs[i * ldg + c] : (i == c ? 1.0 : 0.0);
+      if (i == c && i < b) g += shift;
+    } else {
+      g = (c - B == i) ? 1.0 : 0.0;
+    }
+    w[q] = g;
   }
   bool bad = false;
-#pragma unroll
   for (int j = 0; j < B; ++j) {
-    const double djj = __shfl_sync(0xffffffffu, a[j], j);
-    bad |= !(djj > 0.0) || !isfinite(djj);
-    const double rjj = sqrt(djj);
-    const double rj = (lane < j) ? 0.0 : ((lane == j) ? rjj : a[j] / rjj);
-    a[j] = rj;  // R[j][lane]
+    if (i == j && (j >> 3) == (tid & 7)) {
 #pragma unroll
-    for (int i = j + 1; i < B; ++i) {
-      const double rji = __shfl_sync(0xffffffffu, rj, i);
-      if (lane >= i) a[i] = fma(-rji, rj, a[i]);
+      for (int q = 0; q < 8; ++q)
+        if (cb + q == j) *piv = w[q];
     }
-  }
-  // column `lane` of R^-1 by back substitution (row k of R from lanes >= k)
+    __syncthreads();
+    const double d = *piv;
+    bad |= !(d > 0.0) || !isfinite(d);
+    if (i == j) {
+      // one reciprocal square root on the step's latency chain (as the
+      // cluster Cholesky, chol_cluster.cuh) instead of a sqrt and a division
+      const double ri = rsqrt(d), r = d * ri;
 #pragma unroll
-  for (int k = B - 1; k >= 0; --k) {
-    const double rkk = __shfl_sync(0xffffffffu, a[k], k);
-    double s = 0.0;
-#pragma unroll
-    for (int i = k + 1; i < B; ++i) {
-      const double rki = __shfl_sync(0xffffffffu, a[k], i);
-      if (i <= lane) s = fma(rki, x[i], s);
+      for (int q = 0; q < 8; ++q) {
+        const int c = cb + q;
+        if (c == j) w[q] = r;
+        else if (c > j) w[q] *= ri;
+        rowj[c] = w[q];
+      }
     }
-    x[k] = (k == lane) ? 1.0 / rkk : ((k < lane) ? -s / rkk : 0.0);
+    __syncthreads();
+    if (i > j) {
+      const double a = rowj[i];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (cb + q > j) w[q] = fma(-a, rowj[cb + q], w[q]);
+    }
   }
   double pr = 0.0, pi = 0.0;
-  if (lane < b) {
 #pragma unroll
-    for (int k = 0; k < B; ++k)
-      if (k <= lane) {
-        pr = fma(a[k], a[k], pr);
-        pi = fma(x[k], x[k], pi);
-      }
+  for (int q = 0; q < 8; ++q) {
+    const int c = cb + q;
+    W[i * LDA + c] = w[q];
+    if (i < b && c < b && c >= i) pr = fma(w[q], w[q], pr);                   // R (upper)
+    if (i < b && c >= B && c - B < b && c - B <= i) pi = fma(w[q], w[q], pi);  // R^-T (lower)
   }
-  nr2 = warp_sum(pr);
-  ni2 = warp_sum(pi);
-  return !__any_sync(0xffffffffu, bad);
+  pr = warp_sum(pr);
+  pi = warp_sum(pi);
+  const int lane = tid & 31, warp = tid >> 5;
+  if (lane == 0) {
+    red[warp] = pr;
+    red[NW + warp] = pi;
+  }
+  __syncthreads();
+  nr2 = 0.0;
+  ni2 = 0.0;
+  for (int ww = 0; ww < NW; ++ww) {
+    nr2 += red[ww];
+    ni2 += red[NW + ww];
+  }
+  __syncthreads();
+  return !bad;
 }
 
-// One CholeskyQR step decision for the Gram G (smem, b x b, ld ldg), by
-// warp 0 of the last CTA: cholqr_multi's rule (corutv_b200.cu) -- plain
-// factor if it exists with kappa_F <= kappa_max, else G + s I with s =
-// shift_coeff * tr(G); R^-1 -> st->rinv, state updated.
+// One CholeskyQR step decision for the Gram G (smem, b x b, ld ldg), by the
+// whole last CTA: cholqr_multi's rule (corutv_b200.cu) -- plain factor if
+// it exists with kappa_F <= kappa_max, else G + s I with s = shift_coeff *
+// tr(G); R^-1 -> st->rinv ([k][c] upper), state updated.  W: smem 32 x LDA.
 __device__ void factor_step(const double* Gs, int ldg, int b, double shift_coeff, double kappa_max,
-                            QrState* st) {
-  const int lane = threadIdx.x & 31;
+                            QrState* st, double* W, double* red, double* rowj, double* piv) {
+  const int tid = threadIdx.x;
   double tr = 0.0;
-  for (int i = lane; i < b; i += 32) tr += Gs[i * ldg + i];
-  tr = warp_sum(tr);
-  double x[B];
+  for (int i = 0; i < b; ++i) tr += Gs[i * ldg + i];  // same order in every thread
   int shifted = 0, status = 0;
   double kappa = 1.0;
+  bool ident = false;
   if (!(tr > 0.0) || !isfinite(tr)) {
     // exactly zero input: R = I, Q = X, done (cholqr_multi's status 1); or garbage
-#pragma unroll
-    for (int k = 0; k < B; ++k) x[k] = (k == lane) ? 1.0 : 0.0;
+    ident = true;
     status = isfinite(tr) ? 1 : 2;
   } else {
     double nr2, ni2;
-    bool ok = warp_chol_inv(Gs, ldg, b, 0.0, x, nr2, ni2);
+    bool ok = cta_chol_aug(Gs, ldg, b, 0.0, W, red, rowj, piv, nr2, ni2);
     kappa = sqrt(nr2) * sqrt(ni2);
     if (!ok || !(kappa <= kappa_max)) {
       shifted = 1;
-      ok = warp_chol_inv(Gs, ldg, b, shift_coeff * tr, x, nr2, ni2);
+      ok = cta_chol_aug(Gs, ldg, b, shift_coeff * tr, W, red, rowj, piv, nr2, ni2);
       kappa = sqrt(nr2) * sqrt(ni2);
       if (!ok) status = 2;
     }
   }
-#pragma unroll
-  for (int k = 0; k < B; ++k) st->rinv[k * B + lane] = x[k];
-  if (lane == 0) {
+  // R^-1[k][c] = (R^-T)[c][k]
+  for (int e = tid; e < B * B; e += THREADS) {
+    const int k = e / B, c = e % B;
+    st->rinv[e] = ident ? (k == c ? 1.0 : 0.0) : ((k <= c) ? W[c * LDA + B + k] : 0.0);
+  }
+  if (tid == 0) {
     st->kappa = kappa;
-    st->steps += 1;
+    st->steps = __ldcg(&st->steps) + 1;
     if (status == 2) {
       st->status = 2;
       st->done = 1;
     } else {
-      st->plain = shifted ? 0 : st->plain + 1;
-      st->finish = (status == 1 || st->plain == 2) ? 1 : 0;
+      const int plain = shifted ? 0 : __ldcg(&st->plain) + 1;
+      st->plain = plain;
+      st->finish = (status == 1 || plain == 2) ? 1 : 0;
     }
   }
 }
 
 // lambda_max of the symmetric b x b matrix in smem (ld ldg): warp 0 reduces
-// it to tridiagonal form in registers (lane = column; dsytd2 / dlarfg
-// conventions, zero-padded to 32), then all THREADS evaluate Sturm counts
+// it to tridiagonal form (dsytd2 / dlarfg conventions, zero-padded to 32,
+// matrix in smem W, lane = column), then all THREADS evaluate Sturm counts
 // at THREADS shifts per round (8 bits) from the Gershgorin bracket.
-__device__ double sym_lmax(const double* Gs, int ldg, int b, double* d, double* e, double* xs, int* cs) {
+// vs, wsv: smem scratch vectors of B.
+__device__ double sym_lmax(const double* Gs, int ldg, int b, double* d, double* e, double* xs, int* cs, double* W,
+                           double* vs, double* wsv) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (warp == 0) {
-    double a[B];
-#pragma unroll
-    for (int i = 0; i < B; ++i) a[i] = (i < b && lane < b) ? Gs[i * ldg + lane] : 0.0;
-#pragma unroll
+    for (int i = 0; i < B; ++i) W[i * LDW + lane] = (i < b && lane < b) ? Gs[i * ldg + lane] : 0.0;
+    __syncwarp();
     for (int k = 0; k + 2 < B; ++k) {
-      // x = A[k+1:, k] (column k = lane k's registers), broadcast
-      double xv[B];
-      double sigma = 0.0;
-#pragma unroll
-      for (int i = k + 1; i < B; ++i) {
-        xv[i] = __shfl_sync(0xffffffffu, a[i], k);
-        if (i > k + 1) sigma = fma(xv[i], xv[i], sigma);
-      }
-      const double akk = __shfl_sync(0xffffffffu, a[k], k);
-      const double alpha = xv[k + 1];
+      const double xl = W[lane * LDW + k];  // A[lane][k]
+      const double sigma = warp_sum(lane > k + 1 ? xl * xl : 0.0);
+      const double akk = W[k * LDW + k];
+      const double alpha = W[(k + 1) * LDW + k];
       if (sigma == 0.0) {
         if (lane == 0) {
           d[k] = akk;
@@ -173,34 +210,32 @@ __device__ double sym_lmax(const double* Gs, int ldg, int b, double* d, double* 
       const double beta = (alpha >= 0.0) ? -nrm : nrm;
       const double tau = (beta - alpha) / beta;
       const double scal = 1.0 / (alpha - beta);
-      double v[B];
-#pragma unroll
-      for (int i = 0; i < B; ++i) v[i] = (i == k + 1) ? 1.0 : ((i > k + 1) ? xv[i] * scal : 0.0);
-      // p_c = tau sum_i A[i][c] v_i (column c = row c: symmetric), w = p - (tau/2)(p'v) v
+      const double vl = (lane == k + 1) ? 1.0 : ((lane > k + 1) ? xl * scal : 0.0);
+      vs[lane] = vl;
+      __syncwarp();
+      // p = tau A22 v (column lane = row lane: symmetric), w = p - (tau/2)(p'v) v
       double pc = 0.0;
-#pragma unroll
-      for (int i = k + 1; i < B; ++i) pc = fma(a[i], v[i], pc);
+#pragma unroll 4
+      for (int i = k + 1; i < B; ++i) pc = fma(W[i * LDW + lane], vs[i], pc);
       pc *= tau;
-      const double vc = (lane == k + 1) ? 1.0 : ((lane > k + 1) ? a[k] * scal : 0.0);
-      const double kk = -0.5 * tau * warp_sum((lane > k) ? pc * vc : 0.0);
-      const double wc = fma(kk, vc, pc);
-#pragma unroll
-      for (int i = k + 1; i < B; ++i) {
-        const double wi = __shfl_sync(0xffffffffu, wc, i);
-        if (lane > k) a[i] -= v[i] * wc + wi * vc;
+      const double kk = -0.5 * tau * warp_sum((lane > k) ? pc * vl : 0.0);
+      const double wl = fma(kk, vl, pc);
+      wsv[lane] = wl;
+      __syncwarp();
+      if (lane > k) {
+#pragma unroll 4
+        for (int i = k + 1; i < B; ++i) W[i * LDW + lane] -= vs[i] * wl + wsv[i] * vl;
       }
+      __syncwarp();
       if (lane == 0) {
         d[k] = akk;
         e[k] = beta;
       }
     }
-    const double d30 = __shfl_sync(0xffffffffu, a[B - 2], B - 2);
-    const double e30 = __shfl_sync(0xffffffffu, a[B - 1], B - 2);
-    const double d31 = __shfl_sync(0xffffffffu, a[B - 1], B - 1);
     if (lane == 0) {
-      d[B - 2] = d30;
-      e[B - 2] = e30;
-      d[B - 1] = d31;
+      d[B - 2] = W[(B - 2) * LDW + B - 2];
+      e[B - 2] = W[(B - 1) * LDW + B - 2];
+      d[B - 1] = W[(B - 1) * LDW + B - 1];
     }
   }
   __syncthreads();
@@ -221,7 +256,6 @@ __device__ double sym_lmax(const double* Gs, int ldg, int b, double* d, double* 
     double q = d[0] - x;
     if (fabs(q) < pivmin) q = -pivmin;
     cnt += (q < 0.0);
-#pragma unroll
     for (int i = 1; i < B; ++i) {
       q = (d[i] - x) - e[i - 1] * e[i - 1] / q;
       if (fabs(q) < pivmin) q = -pivmin;
@@ -249,91 +283,219 @@ __device__ double sym_lmax(const double* Gs, int ldg, int b, double* d, double* 
   return 0.5 * (lo + hi);
 }
 
-// Gram of the CTA's rows: lane i of every warp accumulates G[i][.] over the
-// warp's rows (row values broadcast by shuffles), then the warps' partials
-// are summed in warp order into part[blockIdx.x] (b x b, ld b).
-struct GramAcc {
-  double g[B];
-  __device__ void zero() {
-#pragma unroll
-    for (int j = 0; j < B; ++j) g[j] = 0.0;
-  }
-  __device__ void add(double xi) {  // xi = row value of column `lane`
-#pragma unroll
-    for (int j = 0; j < B; ++j) g[j] = fma(xi, __shfl_sync(0xffffffffu, xi, j), g[j]);
-  }
-};
+// Two-level deterministic reduction of the gridDim.x per-CTA Gram partials
+// (32 x 32, ld B, symmetric; only the upper triangle of the leading b x b
+// block is summed): the last CTA of each group of GS (atomic ticket) sums
+// its group in CTA order into part2[group]; the last group reducer sums the
+// groups in order into Gs (smem, 32 x 32, both triangles, zero past b) and
+// returns true; every other CTA returns false.  A thread's loads (all its
+// entries x all CTAs of a group) are issued before any add.
+constexpr int UMAX = (B * (B + 1) / 2 + THREADS - 1) / THREADS;  // upper entries per thread
 
-// the warps' Grams summed in warp order (deterministic) in smem gs (B x B+1),
-// then stored as this CTA's partial part[blockIdx.x] (b x b, ld b)
-__device__ void cta_gram_store(const GramAcc& acc, int b, double* gs, double* part) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int w = 0; w < NW; ++w) {
-    if (warp == w && lane < b)
-#pragma unroll
-      for (int j = 0; j < B; ++j)
-        if (j < b) gs[lane * (B + 1) + j] = (w == 0 ? 0.0 : gs[lane * (B + 1) + j]) + acc.g[j];
-    __syncthreads();
+__device__ __forceinline__ void upper_ij(int u, int b, int* i, int* j) {
+  // u-th entry of the row-major upper triangle of a b x b matrix
+  int r = 0, rem = u;
+  while (rem >= b - r) {
+    rem -= b - r;
+    ++r;
   }
-  for (int e = threadIdx.x; e < b * b; e += THREADS) part[(int64_t)blockIdx.x * b * b + e] = gs[(e / b) * (B + 1) + e % b];
+  *i = r;
+  *j = r + rem;
 }
 
-// last CTA to arrive (atomic ticket): sums the gridDim.x partials in CTA
-// order into Gs (smem, ld b).  Returns false in every other CTA.
-__device__ bool last_cta_reduce(const double* part, int b, unsigned* ticket, double* Gs) {
+__device__ bool last_cta_reduce(const double* part, double* part2, int b, unsigned* tickets, double* Gs) {
   __shared__ int am_last;
+  constexpr int bb = B * B;
+  const int nu = b * (b + 1) / 2;
+  const int group = blockIdx.x / GS, ngroups = (gridDim.x + GS - 1) / GS;
+  const int gsize = min(GS, (int)gridDim.x - group * GS);
+  int idx[UMAX];
+#pragma unroll
+  for (int q = 0; q < UMAX; ++q) {
+    const int u = threadIdx.x + q * THREADS;
+    int i = 0, j = 0;
+    if (u < nu) upper_ij(u, b, &i, &j);
+    idx[q] = (u < nu) ? i * B + j : -1;
+  }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) am_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  if (threadIdx.x == 0) am_last = (atomicAdd(&tickets[1 + group], 1u) == (unsigned)gsize - 1);
   __syncthreads();
   if (!am_last) return false;
   __threadfence();
-  const int bb = b * b;
-  for (int e = threadIdx.x; e < bb; e += THREADS) {
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int c = 0;
-    const int nc = gridDim.x;
-    for (; c + 4 <= nc; c += 4) {
-      s0 += part[(int64_t)c * bb + e];
-      s1 += part[(int64_t)(c + 1) * bb + e];
-      s2 += part[(int64_t)(c + 2) * bb + e];
-      s3 += part[(int64_t)(c + 3) * bb + e];
+  {
+    double v[UMAX][GS];
+#pragma unroll
+    for (int q = 0; q < UMAX; ++q)
+#pragma unroll
+      for (int c = 0; c < GS; ++c)
+        v[q][c] = (idx[q] >= 0 && c < gsize) ? __ldcg(part + (int64_t)(group * GS + c) * bb + idx[q]) : 0.0;
+#pragma unroll
+    for (int q = 0; q < UMAX; ++q) {
+      double sum = 0.0;
+#pragma unroll
+      for (int c = 0; c < GS; ++c) sum += v[q][c];
+      if (idx[q] >= 0) {
+        if (ngroups == 1) Gs[idx[q]] = sum;
+        else part2[(int64_t)group * bb + idx[q]] = sum;
+      }
     }
-    for (; c < nc; ++c) s0 += part[(int64_t)c * bb + e];
-    Gs[e] = (s0 + s1) + (s2 + s3);
   }
-  if (threadIdx.x == 0) *ticket = 0;
+  if (threadIdx.x == 0) tickets[1 + group] = 0;
+  if (ngroups > 1) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) am_last = (atomicAdd(&tickets[0], 1u) == (unsigned)ngroups - 1);
+    __syncthreads();
+    if (!am_last) return false;
+    __threadfence();
+    double v[UMAX][GS];
+#pragma unroll
+    for (int q = 0; q < UMAX; ++q)
+#pragma unroll
+      for (int g = 0; g < GS; ++g) v[q][g] = (idx[q] >= 0 && g < ngroups) ? __ldcg(part2 + (int64_t)g * bb + idx[q]) : 0.0;
+#pragma unroll
+    for (int q = 0; q < UMAX; ++q) {
+      double sum = 0.0;
+#pragma unroll
+      for (int g = 0; g < GS; ++g) sum += v[q][g];
+      if (idx[q] >= 0) Gs[idx[q]] = sum;
+    }
+    if (threadIdx.x == 0) tickets[0] = 0;
+  }
+  __syncthreads();
+  // mirror to the lower triangle, zero outside the b x b block
+  for (int e = threadIdx.x; e < bb; e += THREADS) {
+    const int i = e / B, j = e % B;
+    if (i >= b || j >= b) Gs[e] = 0.0;
+    else if (i > j) Gs[e] = Gs[j * B + i];
+  }
   __syncthreads();
   return true;
 }
 
-struct Smem {
-  double gs[B * (B + 1)];
-  double G[B * B];
-  double d[B], e[B];
-  double xs[THREADS];
-  int cs[NW];
-};
-
 // rows [r0, r1) of this CTA (contiguous chunks)
 __device__ __forceinline__ void cta_rows(int64_t rows, int64_t* r0, int64_t* r1) {
   const int64_t chunk = (rows + gridDim.x - 1) / gridDim.x;
-  *r0 = min<int64_t>(rows, (int64_t)blockIdx.x * chunk);
-  *r1 = min<int64_t>(rows, *r0 + chunk);
+  const int64_t a = (int64_t)blockIdx.x * chunk;
+  *r0 = a < rows ? a : rows;
+  *r1 = *r0 + chunk < rows ? *r0 + chunk : rows;
+}
+
+// The row kernels stage RCH rows at a time in shared memory (row stride
+// LDX, columns b..31 and rows past the end zero): every global access is a
+// coalesced sweep by the whole CTA, and the CTA's Gram partial is formed on
+// the tensor pipe (DMMA.884: 16 8x8 blocks of the padded 32 x 32 Gram, two
+// per warp, K = the chunk's rows).
+constexpr int RCH = 96;
+constexpr int LDX = 36;
+
+struct RowSmem {
+  union {
+    double x[RCH * LDX];
+    struct {
+      double G[B * B];
+      double W[B * LDA];
+    } f;
+  } u;
+  double Ri[B * (B + 1)];
+  double red[2 * NW];
+  double rowj[2 * B];
+  double piv[2];
+};
+
+__device__ __forceinline__ void gram_chunk(const double* x, int nr4, double (&acc)[2][2]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r8 = lane >> 2, c4 = lane & 3;
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int q = 2 * warp + t, bi = q >> 2, bj = q & 3;
+    for (int k0 = 0; k0 < nr4; k0 += 4) {
+      const double a = x[(k0 + c4) * LDX + bi * 8 + r8];
+      const double bb = x[(k0 + c4) * LDX + bj * 8 + r8];
+      dmma884(acc[t][0], acc[t][1], a, bb);
+    }
+  }
+}
+
+__device__ __forceinline__ void gram_store(const double (&acc)[2][2], double* part) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r8 = lane >> 2, c4 = lane & 3;
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int q = 2 * warp + t, bi = q >> 2, bj = q & 3;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) part[(int64_t)blockIdx.x * B * B + (bi * 8 + r8) * B + bj * 8 + 2 * c4 + e] = acc[t][e];
+  }
+}
+
+// x (RCH x 32 in smem, zero past nr / b) <- x R^-1 (Ri: smem [k][c] upper,
+// ld B + 1) in place, on the tensor pipe: 12 x 4 output blocks of 8 x 8
+// (K = 32), six per warp, held in registers until every warp has read x
+__device__ __forceinline__ void apply_rinv_chunk(double* x, const double* Ri, int nr4) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r8 = lane >> 2, c4 = lane & 3;
+  constexpr int NBLK = (RCH / 8) * (B / 8);       // 48
+  constexpr int PERW = NBLK / NW;                 // 6
+  double o[PERW][2];
+#pragma unroll
+  for (int t = 0; t < PERW; ++t) {
+    const int q = warp * PERW + t, bi = q / (B / 8), bj = q % (B / 8);
+    o[t][0] = o[t][1] = 0.0;
+    if (bi * 8 < nr4) {
+#pragma unroll
+      for (int k0 = 0; k0 < B; k0 += 4) {
+        const double a = x[(bi * 8 + r8) * LDX + k0 + c4];
+        const double bb = Ri[(k0 + c4) * (B + 1) + bj * 8 + r8];
+        dmma884(o[t][0], o[t][1], a, bb);
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < PERW; ++t) {
+    const int q = warp * PERW + t, bi = q / (B / 8), bj = q % (B / 8);
+    if (bi * 8 < nr4) {
+      x[(bi * 8 + r8) * LDX + bj * 8 + 2 * c4] = o[t][0];
+      x[(bi * 8 + r8) * LDX + bj * 8 + 2 * c4 + 1] = o[t][1];
+    }
+  }
+  __syncthreads();
+}
+
+// write the chunk to out (rows, ld ldo; coalesced along columns) and outT
+// (b x rows, ld ldoT; coalesced along rows)
+__device__ __forceinline__ void store_chunk(const double* x, int nr, int b, int64_t row0, double* out, int64_t ldo,
+                                            double* outT, int64_t ldoT) {
+  for (int e = threadIdx.x; e < nr * b; e += THREADS) {
+    const int r = e / b, c = e % b;
+    out[(row0 + r) * ldo + c] = x[r * LDX + c];
+  }
+  if (outT)
+    for (int e = threadIdx.x; e < nr * b; e += THREADS) {
+      const int c = e / nr, r = e % nr;
+      outT[(int64_t)c * ldoT + row0 + r] = x[r * LDX + c];
+    }
 }
 
 // MODE 0 (w = A v): finalize w from the split-K partials (ws, `splits`
-// slices of stride sstride, ld ldw) into out (ld ldo), Gram, last CTA:
-// lam[0] = lambda_max(w'w).
-// MODE 1 (z = A' w): finalize z into out (the CholeskyQR buffer), Gram,
-// last CTA: first factor step into st.
+// slices of stride sstride, ld ldw), times the pending R^-1 of the previous
+// CholeskyQR (its last apply folded in: A (v' R^-1) = (A v') R^-1;
+// identity on the first iteration), into out (+ outT); Gram; the last CTA
+// writes the reduced Gram w'w (32 x 32, padded) to lam for lmax_kernel.
+// MODE 1 (z = A' w): finalize z into out (the CholeskyQR buffer) + outT;
+// Gram; the last CTA takes the first factor step into st.
 template <int MODE>
 __global__ void __launch_bounds__(THREADS, 1)
     finalize_kernel(const double* __restrict__ ws, int splits, int64_t sstride, int64_t ldw, int64_t rows, int b,
-                    double* __restrict__ out, int64_t ldo, double* __restrict__ part, unsigned* ticket,
-                    double* lam, QrState* st, double shift_coeff, double kappa_max) {
-  __shared__ Smem sm;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+                    double* __restrict__ out, int64_t ldo, double* __restrict__ outT, int64_t ldoT,
+                    double* __restrict__ part, double* __restrict__ part2, unsigned* tickets, double* lam,
+                    QrState* st, double shift_coeff, double kappa_max, int use_pending) {
+  __shared__ RowSmem sm;
+  if (MODE == 0) {
+    for (int e = threadIdx.x; e < B * B; e += THREADS)
+      sm.Ri[(e / B) * (B + 1) + e % B] = use_pending ? __ldcg(st->rinv + e) : ((e / B == e % B) ? 1.0 : 0.0);
+  }
   if (MODE == 1 && blockIdx.x == 0 && threadIdx.x == 0) {
     // fresh CholeskyQR state (visible to the apply launches after this one)
     st->plain = 0;
@@ -344,94 +506,118 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   int64_t r0, r1;
   cta_rows(rows, &r0, &r1);
-  GramAcc acc;
-  acc.zero();
-  for (int64_t r = r0 + warp; r < r1; r += NW) {
-    double v = 0.0;
-    if (lane < b) {
-      const double* src = ws + r * ldw + lane;
-      int s = 0;
-      for (; s + 4 <= splits; s += 4) {
-        const double p0 = src[(int64_t)s * sstride], p1 = src[(int64_t)(s + 1) * sstride];
-        const double p2 = src[(int64_t)(s + 2) * sstride], p3 = src[(int64_t)(s + 3) * sstride];
-        v += p0;
-        v += p1;
-        v += p2;
-        v += p3;
-      }
-      for (; s < splits; ++s) v += src[(int64_t)s * sstride];
-      out[r * ldo + lane] = v;
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  for (int64_t c0 = r0; c0 < r1; c0 += RCH) {
+    const int nr = (int)min((int64_t)RCH, r1 - c0), nr4 = (nr + 3) & ~3;
+    // zero the padding (rows nr..nr4, columns b..32), then the split-K sum
+    // of the nr x b elements in fixed order: per thread 4 elements x up to
+    // 16 slices of loads in flight before any add
+    for (int e = threadIdx.x; e < nr4 * B; e += THREADS) {
+      const int r = e / B, c = e % B;
+      if (r >= nr || c >= b) sm.u.x[r * LDX + c] = 0.0;
     }
-    acc.add(v);
+    const int ne = nr * b;
+    for (int e0 = threadIdx.x; e0 < ne; e0 += 4 * THREADS) {
+      int64_t off[4];
+      int sidx[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int e = e0 + k * THREADS, r = e / b, c = e % b;
+        off[k] = (c0 + r) * ldw + c;
+        sidx[k] = (e < ne) ? r * LDX + c : -1;
+      }
+      double v[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int s0 = 0; s0 < splits; s0 += 16) {
+        double p[16][4];
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            p[q][k] = (sidx[k] >= 0 && s0 + q < splits) ? __ldcg(ws + (int64_t)(s0 + q) * sstride + off[k]) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (s0 + q < splits) v[k] += p[q][k];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (sidx[k] >= 0) sm.u.x[sidx[k]] = v[k];
+    }
+    __syncthreads();
+    if (MODE == 0) apply_rinv_chunk(sm.u.x, sm.Ri, nr4);
+    store_chunk(sm.u.x, nr, b, c0, out, ldo, outT, ldoT);
+    gram_chunk(sm.u.x, nr4, acc);
+    __syncthreads();
   }
-  cta_gram_store(acc, b, sm.gs, part);
-  if (!last_cta_reduce(part, b, ticket, sm.G)) return;
+  gram_store(acc, part);
+  if (!last_cta_reduce(part, part2, b, tickets, sm.u.f.G)) return;
   if (MODE == 0) {
-    const double l = sym_lmax(sm.G, b, b, sm.d, sm.e, sm.xs, sm.cs);
-    if (threadIdx.x == 0) lam[0] = l;
+    for (int e = threadIdx.x; e < B * B; e += THREADS) lam[e] = sm.u.f.G[e];
   } else {
-    if (warp == 0) factor_step(sm.G, b, b, shift_coeff, kappa_max, st);
+    factor_step(sm.u.f.G, B, b, shift_coeff, kappa_max, st, sm.u.f.W, sm.red, sm.rowj, sm.piv);
   }
 }
 
-// One CholeskyQR apply: x <- x R^-1 in place (rows x b, ld ldx) and the
-// transposed copy xT (b x rows, ld ldxT); unless this was the last step,
-// the Gram of the new rows and, in the last CTA, the next factor.
+struct LmaxSmem {
+  double G[B * B];
+  double W[B * LDW];
+  double d[B], e[B];
+  double xs[THREADS];
+  int cs[NW];
+  double vs[B], wsv[B];
+};
+
+// lambda_max of the b x b Gram G (global, ld ldg) -> lam[0]; one CTA.
+__global__ void __launch_bounds__(THREADS, 1) lmax_kernel(const double* __restrict__ G, int ldg, int b, double* lam) {
+  __shared__ LmaxSmem sm;
+  for (int e = threadIdx.x; e < b * b; e += THREADS) sm.G[e] = G[(e / b) * ldg + e % b];
+  __syncthreads();
+  const double l = sym_lmax(sm.G, b, b, sm.d, sm.e, sm.xs, sm.cs, sm.W, sm.vs, sm.wsv);
+  if (threadIdx.x == 0) lam[0] = l;
+}
+
+// One CholeskyQR apply: x <- x R^-1 in place (rows x b, ld ldx) with the
+// pending factor, plus the transposed copy xT (b x rows, ld ldxT), the Gram
+// of the new rows and, in the last CTA, the next factor.  Returns at once
+// when the pending factor is the final one (the next finalize_kernel<0>
+// applies it) or on an error status.
 __global__ void __launch_bounds__(THREADS, 1)
     apply_kernel(double* __restrict__ x, int64_t ldx, double* __restrict__ xT, int64_t ldxT, int64_t rows, int b,
-                 double* __restrict__ part, QrState* st, double shift_coeff, double kappa_max, int last_launch) {
-  __shared__ Smem sm;
-  __shared__ double Ri[B * (B + 1)];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (*((volatile int*)&st->done)) return;  // uniform: written by an earlier launch
-  const bool finish = *((volatile int*)&st->finish) != 0;
-  for (int e = threadIdx.x; e < B * B; e += THREADS) Ri[(e / B) * (B + 1) + e % B] = st->rinv[e];
-  __syncthreads();
+                 double* __restrict__ part, double* __restrict__ part2, QrState* st, double shift_coeff,
+                 double kappa_max, int last_launch) {
+  __shared__ RowSmem sm;
+  if (*((volatile int*)&st->finish) || *((volatile int*)&st->status)) return;  // uniform: earlier launches
+  for (int e = threadIdx.x; e < B * B; e += THREADS) sm.Ri[(e / B) * (B + 1) + e % B] = __ldcg(st->rinv + e);
   int64_t r0, r1;
   cta_rows(rows, &r0, &r1);
-  GramAcc acc;
-  acc.zero();
-  for (int64_t r = r0 + warp; r < r1; r += NW) {
-    const double xi = (lane < b) ? x[r * ldx + lane] : 0.0;
-    double o = 0.0;
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  for (int64_t c0 = r0; c0 < r1; c0 += RCH) {
+    const int nr = (int)min((int64_t)RCH, r1 - c0), nr4 = (nr + 3) & ~3;
+    constexpr int PER = (RCH * B + THREADS - 1) / THREADS;  // 12: all loads in flight
+    double xv[PER];
 #pragma unroll
-    for (int k = 0; k < B; ++k) {
-      const double xk = __shfl_sync(0xffffffffu, xi, k);
-      if (k <= lane) o = fma(xk, Ri[k * (B + 1) + lane], o);
+    for (int q = 0; q < PER; ++q) {
+      const int e = threadIdx.x + q * THREADS, r = e / B, c = e % B;
+      xv[q] = (r < nr && c < b) ? x[(c0 + r) * ldx + c] : 0.0;
     }
-    if (lane < b) {
-      x[r * ldx + lane] = o;
-      xT[(int64_t)lane * ldxT + r] = o;
-    } else {
-      o = 0.0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = threadIdx.x + q * THREADS, r = e / B, c = e % B;
+      if (r < nr4) sm.u.x[r * LDX + c] = xv[q];
     }
-    if (!finish) acc.add(o);
-  }
-  if (finish) {
-    // the last CTA to finish marks the state done: every CTA of this launch
-    // has passed its `done` check by then
-    __shared__ int am_last;
-    __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) am_last = (atomicAdd(&st->ticket, 1u) == gridDim.x - 1);
+    apply_rinv_chunk(sm.u.x, sm.Ri, nr4);
+    store_chunk(sm.u.x, nr, b, c0, x, ldx, xT, ldxT);
+    gram_chunk(sm.u.x, nr4, acc);
     __syncthreads();
-    if (am_last && threadIdx.x == 0) {
-      st->ticket = 0;
-      st->finish = 0;
-      st->done = 1;
-    }
-    return;
   }
-  cta_gram_store(acc, b, sm.gs, part);
-  if (!last_cta_reduce(part, b, &st->ticket, sm.G)) return;
-  if (warp == 0) {
-    factor_step(sm.G, b, b, shift_coeff, kappa_max, st);
-    // the launch budget is spent and another step would be needed
-    if (lane == 0 && last_launch && !st->finish && st->status == 0) {
-      st->status = 3;
-      st->done = 1;
-    }
-  }
+  gram_store(acc, part);
+  if (!last_cta_reduce(part, part2, b, st->tickets, sm.u.f.G)) return;
+  factor_step(sm.u.f.G, B, b, shift_coeff, kappa_max, st, sm.u.f.W, sm.red, sm.rowj, sm.piv);
+  __syncthreads();
+  // the launch budget is spent and another step would be needed
+  if (threadIdx.x == 0 && last_launch && !__ldcg(&st->finish) && __ldcg(&st->status) == 0) st->status = 3;
 }
 
 }  // namespace sn
