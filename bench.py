@@ -456,7 +456,9 @@ def main():
     omega_host = P.gaussian_matrix(n, ell, 0)
     omega = torch.from_numpy(omega_host).to(device)
     cfg = P.SketchConfig(ell=ell, q_power=q, seed=0)
-    comm = RowShardComm() if world > 1 else None
+    # NCCL ranks: the library's own communicator (every exchange an
+    # ncclAllReduce on its stream); the gloo dry run keeps the callback
+    comm = RowShardComm(native=(backend == "nccl")) if world > 1 else None
     h = _lib.handle(local)
 
     def step(x, om):

@@ -68,15 +68,18 @@ int corutv_set_comm(corutv_handle* h, corutv_allreduce_fn fn, void* user, int ra
  * sketch, the ell x ell core, the spectral norm's Gram and n x b block, the
  * ALM scalars) is an ncclAllReduce enqueued by the library on the handle's
  * stream -- no host callback, no host synchronisation of its own.
- *   corutv_nccl_unique_id : rank 0 creates the 128-byte ncclUniqueId (the
- *                           host layer broadcasts it, e.g. over its store);
- *   corutv_nccl_init      : every rank joins (ncclCommInitRank); the handle
- *                           owns the communicator;
- *   corutv_set_nccl       : attach a caller-owned ncclComm_t (NULL detaches).
+ *   corutv_nccl_unique_id     : rank 0 creates the 128-byte ncclUniqueId
+ *                               (the host layer broadcasts it);
+ *   corutv_nccl_comm_create   : every rank joins (ncclCommInitRank on
+ *                               `device`); the caller owns the ncclComm_t;
+ *   corutv_nccl_comm_destroy  : ncclCommDestroy;
+ *   corutv_set_nccl           : attach a communicator to a handle for the
+ *                               following calls (NULL detaches).
  * NCCL (libnccl.so.2) is resolved at run time.  A one-rank communicator
  * runs the sharded code path on one GPU.  corutv_set_comm detaches it. */
 int corutv_nccl_unique_id(unsigned char* id_out);
-int corutv_nccl_init(corutv_handle* h, const unsigned char* id, int rank, int world);
+int corutv_nccl_comm_create(int device, const unsigned char* id, int rank, int world, void** comm_out);
+int corutv_nccl_comm_destroy(void* nccl_comm);
 int corutv_set_nccl(corutv_handle* h, void* nccl_comm, int rank, int world);
 
 /* Row-sharded mode: the global row count of the matrices of the following

@@ -76,7 +76,8 @@ SIGNATURES = {
     "corutv_shrink": (_I32, [_VP, _VP, _I64, _I64, _I64, _D, _VP, _I64]),
     "corutv_set_global_rows": (_I32, [_VP, _I64]),
     "corutv_nccl_unique_id": (_I32, [_VP]),
-    "corutv_nccl_init": (_I32, [_VP, _VP, _I32, _I32]),
+    "corutv_nccl_comm_create": (_I32, [_I32, _VP, _I32, _I32, ctypes.POINTER(_VP)]),
+    "corutv_nccl_comm_destroy": (_I32, [_VP]),
     "corutv_set_nccl": (_I32, [_VP, _VP, _I32, _I32]),
     "corutv_lowrank_error": (_I32, [_VP, _VP, _I64, _I64, _I64, _VP, _VP, _VP, _I32, c_double_p]),
     "corutv_gemm": (_I32, [_VP, _I32, _I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _I64]),

@@ -1722,7 +1722,10 @@ void spectral_norm_fused(corutv_handle* h, const double* A, int64_t ldA, int64_t
   const int64_t ldb2 = round_up(b, 16), ldnp = round_up(np, 16), ldmp = round_up(mp, 16);
   const int64_t ldw = round_up(b, 2);
   auto ctas = [&](int64_t rows) { return (int)std::max<int64_t>(1, std::min<int64_t>(h->num_sms, (rows + 31) / 32)); };
-  const int gw = ctas(mp), gz = ctas(np);
+  const int gw = ctas(std::max<int64_t>(mp, 1)), gz = ctas(np);
+  // row-sharded (tall): w and its Gram are local (the Gram is all-reduced
+  // before lambda_max); z = A' w is all-reduced before the replicated QR
+  const bool sharded = is_sharded(h);
   Arena ar(h);
   double *vT, *v, *w, *wT = nullptr, *ws, *gpart, *gpart2, *lam;
   sn::QrState* qst;
@@ -1758,7 +1761,7 @@ void spectral_norm_fused(corutv_handle* h, const double* A, int64_t ldA, int64_t
   }
   double prev = 0.0;
   for (int it = 0; it < max_iter; ++it) {
-    GemmPlan pw, pz;
+    GemmPlan pw{}, pz{};
     // w = A' v  (A' = A if tall else A^T), partials -> w (+ w^T), lambda_max(w'w)
     if (tall) run_gemm(h, false, m, b, n, A, ldA, vT, ldnp, nullptr, 0, nullptr, 0, ws, nullptr, nullptr, &pw);
     else run_gemm(h, true, n, b, m, A, ldA, v, ldb2, nullptr, 0, nullptr, 0, ws, nullptr, nullptr, &pw);
@@ -1767,6 +1770,7 @@ void spectral_norm_fused(corutv_handle* h, const double* A, int64_t ldA, int64_t
                                                              gpart, gpart2, wst->tickets, gram_w, qst, 0.0, 0.0,
                                                              it > 0 ? 1 : 0);
     CK_LAUNCH();
+    if (sharded) allreduce(h, gram_w, (int64_t)sn::B * sn::B);
     CK(cudaEventRecord(h->fork_ev, h->stream));
     CK(cudaStreamWaitEvent(h->side, h->fork_ev, 0));
     sn::lmax_kernel<<<1, sn::THREADS, 0, h->side>>>(gram_w, sn::B, b, lam);
@@ -1774,11 +1778,20 @@ void spectral_norm_fused(corutv_handle* h, const double* A, int64_t ldA, int64_t
     CK(cudaMemcpyAsync(h->pinned + 8, lam, sizeof(double), cudaMemcpyDeviceToHost, h->side));
     CK(cudaEventRecord(h->est_ev, h->side));
     // z = A'^T w, partials -> v, CholeskyQR in place
-    if (tall) run_gemm(h, true, n, b, m, A, ldA, w, ldb2, nullptr, 0, nullptr, 0, ws, nullptr, nullptr, &pz);
-    else run_gemm(h, false, m, b, n, A, ldA, wT, ldmp, nullptr, 0, nullptr, 0, ws, nullptr, nullptr, &pz);
-    sn::finalize_kernel<1><<<gz, sn::THREADS, 0, h->stream>>>(ws, pz.splits, np * ldw, ldw, np, b, v, ldb2, vT, ldnp,
-                                                             gpart, gpart2, qst->tickets, nullptr, qst, coeff,
-                                                             kKappaPlain, 0);
+    if (sharded) {
+      // local partial z (finalized into v), summed over the ranks, then
+      // the same Gram + first factor from v itself (one "split")
+      run_gemm(h, true, n, b, m, A, ldA, w, ldb2, v, ldb2, nullptr, 0, ws);
+      allreduce(h, v, np * ldb2);
+      sn::finalize_kernel<1><<<gz, sn::THREADS, 0, h->stream>>>(v, 1, 0, ldb2, np, b, v, ldb2, vT, ldnp, gpart, gpart2,
+                                                               qst->tickets, nullptr, qst, coeff, kKappaPlain, 0);
+    } else {
+      if (tall) run_gemm(h, true, n, b, m, A, ldA, w, ldb2, nullptr, 0, nullptr, 0, ws, nullptr, nullptr, &pz);
+      else run_gemm(h, false, m, b, n, A, ldA, wT, ldmp, nullptr, 0, nullptr, 0, ws, nullptr, nullptr, &pz);
+      sn::finalize_kernel<1><<<gz, sn::THREADS, 0, h->stream>>>(ws, pz.splits, np * ldw, ldw, np, b, v, ldb2, vT,
+                                                               ldnp, gpart, gpart2, qst->tickets, nullptr, qst, coeff,
+                                                               kKappaPlain, 0);
+    }
     CK_LAUNCH();
     // typically: apply R1 + factor 2 (final: the next finalize applies it), no-op
     for (int s = 0; s < kApply; ++s) {
@@ -1811,8 +1824,9 @@ void spectral_norm(corutv_handle* h, const double* a, int64_t m, int64_t n, int6
                    int max_iter, double* out, int* iters) {
   static const bool legacy = std::getenv("CORUTV_SNORM_LEGACY") != nullptr;  // A/B knob
   const bool sharded = is_sharded(h);
-  if (!legacy && !sharded && m >= 1 && n >= 1 && std::min(m, n) > 64) {
-    const bool tall = m >= n;
+  const double mg = sharded ? global_rows(h, m) : (double)m;
+  if (!legacy && m >= (sharded ? 0 : 1) && n >= 1 && std::min(mg, (double)n) > 64 && (!sharded || mg >= n)) {
+    const bool tall = sharded || m >= n;
     const int b = (int)std::min<int64_t>(24, tall ? n : m);
     const bool a_ok = ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && (lda % 2 == 0);
     try {
@@ -2115,24 +2129,28 @@ int corutv_nccl_unique_id(unsigned char* id_out) {
   return CORUTV_OK;
 }
 
-int corutv_nccl_init(corutv_handle* hh, const unsigned char* id, int rank, int world) {
-  ABI_BEGIN(hh)
-  if (!id || world < 1 || rank < 0 || rank >= world) fail(h, CORUTV_ERR_ARG, "bad NCCL rank/world");
+int corutv_nccl_comm_create(int device, const unsigned char* id, int rank, int world, void** comm_out) {
+  if (!id || !comm_out || world < 1 || rank < 0 || rank >= world) return CORUTV_ERR_ARG;
+  *comm_out = nullptr;
   const NcclApi& api = nccl_api();
-  if (!api.ok) fail(h, CORUTV_ERR_COMM, "libnccl.so.2 not found");
-  release_nccl(h);
+  if (!api.ok) return CORUTV_ERR_COMM;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    cudaGetLastError();
+    return CORUTV_ERR_CUDA;
+  }
   ncclUniqueId uid;
   std::memcpy(&uid, id, sizeof(uid));
   ncclComm_t comm = nullptr;
-  const ncclResult_t r = api.comm_init_rank(&comm, world, uid, rank);
-  if (r != ncclSuccess) fail(h, CORUTV_ERR_COMM, std::string("ncclCommInitRank: ") + api.error_string(r));
-  h->nccl = comm;
-  h->nccl_owned = true;
-  h->ar_fn = nullptr;
-  h->rank = rank;
-  h->world = world;
-  h->m_global = 0;
-  ABI_END
+  if (api.comm_init_rank(&comm, world, uid, rank) != ncclSuccess) return CORUTV_ERR_COMM;
+  *comm_out = comm;
+  return CORUTV_OK;
+}
+
+int corutv_nccl_comm_destroy(void* comm) {
+  if (!comm) return CORUTV_OK;
+  const NcclApi& api = nccl_api();
+  if (!api.ok) return CORUTV_ERR_COMM;
+  return api.comm_destroy(reinterpret_cast<ncclComm_t>(comm)) == ncclSuccess ? CORUTV_OK : CORUTV_ERR_COMM;
 }
 
 int corutv_set_nccl(corutv_handle* hh, void* comm, int rank, int world) {

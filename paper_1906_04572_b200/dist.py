@@ -1,8 +1,10 @@
 """Row-sharded (multi-GPU) CoR-UTV — SURVEY §8e.
 
 One process per GPU; rank g owns a contiguous block of rows A_g.  The
-native library does all the math and calls back into this module at the
-exchange points of the algorithm (sum-allreduce on the handle's stream):
+native library does all the math; at the exchange points of the algorithm
+it runs a sum-allreduce on the handle's stream -- ncclAllReduce on its own
+communicator (``RowShardComm(native=True)``), or a callback into this
+module (the gloo test path):
 
   * C2 = sum_g A_g' C1_g                 (n x ell, per power iteration)
   * Gram X'X of the row-sharded Q1 sketch (ell x ell, per CholeskyQR step)
@@ -10,9 +12,7 @@ exchange points of the algorithm (sum-allreduce on the handle's stream):
   * the global row count, the non-finite flag, ALM (zeta^2, nnz) scalars
 
 Everything replicated (Q2, the QRCP of D, V) is computed redundantly and
-bit-identically on every rank from the all-reduced inputs.  The callback is
-bound to ``torch.distributed.all_reduce`` (NCCL over NVLink on GPUs; gloo
-in the CPU tests).
+bit-identically on every rank from the all-reduced inputs.
 """
 
 from __future__ import annotations
@@ -49,11 +49,17 @@ class _CudaBuffer:
 
 
 class RowShardComm:
-    """Sum-allreduce callback for the native library over a torch.distributed
-    process group.  ``device``: "cuda" (pointers are device memory) or
-    "cpu" (host pointers; used by the gloo tests of the marshalling)."""
+    """The row-sharded data plane over a torch.distributed process group.
 
-    def __init__(self, group=None, device: str = "cuda"):
+    ``native=True`` (the production path on GPUs): the library gets its own
+    NCCL communicator (rank 0 creates the id, the group broadcasts it, every
+    rank joins) and enqueues every exchange as ncclAllReduce on its stream
+    -- no Python runs per collective.  ``native=False``: a sum-allreduce
+    callback into ``torch.distributed.all_reduce`` (the gloo test path);
+    ``device``: "cuda" (pointers are device memory) or "cpu" (host
+    pointers; used by the CPU tests of the marshalling)."""
+
+    def __init__(self, group=None, device: str = "cuda", native: bool = False):
         import torch.distributed as tdist
 
         self.group = group
@@ -62,6 +68,38 @@ class RowShardComm:
         self.device = device
         self.calls = 0
         self.callback = _lib.ALLREDUCE_FN(self._allreduce)
+        self.native = native
+        self.nccl = None
+        if native:
+            self._init_nccl()
+
+    def _init_nccl(self):
+        import torch
+        import torch.distributed as tdist
+
+        lib = _lib.load_library()
+        uid = (ctypes.c_ubyte * 128)()
+        if self.rank == 0:
+            _lib.check(lib.corutv_nccl_unique_id(uid), None, "corutv_nccl_unique_id")
+        box = [bytes(uid)]
+        tdist.broadcast_object_list(box, src=tdist.get_global_rank(self.group, 0) if self.group else 0,
+                                    group=self.group)
+        uid = (ctypes.c_ubyte * 128).from_buffer_copy(box[0])
+        comm = ctypes.c_void_p()
+        _lib.check(lib.corutv_nccl_comm_create(torch.cuda.current_device(), uid, self.rank, self.world,
+                                               ctypes.byref(comm)), None, "corutv_nccl_comm_create")
+        self.nccl = comm
+
+    def close(self):
+        if self.nccl:
+            _lib.load_library().corutv_nccl_comm_destroy(self.nccl)
+            self.nccl = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     def _tensor(self, ptr: int, count: int):
         import torch
@@ -94,14 +132,21 @@ class RowShardComm:
         return int(t.item())
 
     def attach(self, handle: "_lib.Handle", global_rows: int | None = None) -> None:
-        _lib.check(handle.lib.corutv_set_comm(handle.ptr, self.callback, None, self.rank, self.world),
-                   handle.ptr, "corutv_set_comm")
+        if self.native:
+            _lib.check(handle.lib.corutv_set_nccl(handle.ptr, self.nccl, self.rank, self.world), handle.ptr,
+                       "corutv_set_nccl")
+        else:
+            _lib.check(handle.lib.corutv_set_comm(handle.ptr, self.callback, None, self.rank, self.world),
+                       handle.ptr, "corutv_set_comm")
         if global_rows is not None:
             _lib.check(handle.lib.corutv_set_global_rows(handle.ptr, int(global_rows)), handle.ptr,
                        "corutv_set_global_rows")
 
     def detach(self, handle: "_lib.Handle") -> None:
-        handle.lib.corutv_set_comm(handle.ptr, _lib.ALLREDUCE_FN(), None, 0, 1)
+        if self.native:
+            handle.lib.corutv_set_nccl(handle.ptr, None, 0, 1)
+        else:
+            handle.lib.corutv_set_comm(handle.ptr, _lib.ALLREDUCE_FN(), None, 0, 1)
 
 
 def corutv_sharded(a_local, cfg: SketchConfig, comm: RowShardComm, counter: PassCounter | None = None,
