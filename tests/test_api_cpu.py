@@ -10,6 +10,9 @@ import pytest
 import oracle as O
 import paper_1906_04572_b200 as P
 from paper_1906_04572_b200 import rpca as R
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
 
 
 def test_sketch_config_validation():
@@ -107,6 +110,33 @@ def test_install_rebinds_reference_names():
         for k in list(sys.modules):
             if k.startswith("fakecorutv"):
                 del sys.modules[k]
+
+
+def test_install_rebinds_the_real_reference_package():
+    """install() against the unmodified reference in baseline/_ref (pip
+    --target, tools/stage_reference.sh): every hot-path name the reference's
+    own modules and tests import resolves to the device implementation."""
+    import subprocess
+    import sys
+
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "corutv" / "__init__.py").exists():
+        pytest.skip("baseline/_ref not staged (tools/stage_reference.sh)")
+    code = (
+        "import sys; sys.path[:0] = [%r, %r]\n"
+        "import corutv, corutv.sketch, corutv.rpca, corutv.bench\n"
+        "assert corutv.__file__.startswith(%r), corutv.__file__\n"
+        "import paper_1906_04572_b200 as P\n"
+        "done = P.install(corutv)\n"
+        "assert corutv.sketch.corutv is P.corutv and corutv.rpca.corutv is P.corutv\n"
+        "assert corutv.bench.corutv is P.corutv and corutv.bench.alm_corutv is P.alm_corutv\n"
+        "assert corutv.rpca.alm_corutv is P.alm_corutv and corutv.rpca.inexact_alm is P.inexact_alm\n"
+        "assert corutv.sketch.sor_svd is P.sor_svd and corutv.sketch.tsr_svd is P.tsr_svd\n"
+        "from corutv.sketch import corutv as c; assert c is P.corutv\n"
+        "print(len(done))\n" % (str(ROOT), str(ref), str(ref)))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    assert int(out.stdout.strip()) >= 10
 
 
 def test_gaussian_matrix_is_the_reference_stream(golden):
