@@ -45,6 +45,35 @@ __all__ = [
 ]
 
 
+def _adopt_reference_errors(errs) -> bool:
+    """Make the exceptions this package raises also instances of the
+    reference's own ``CorutvError`` / ``ConvergenceError`` (errors.py:4-18),
+    so a caller's ``except corutv.errors.ConvergenceError`` (or the
+    reference tests' ``pytest.raises``) catches what the device path raises,
+    with the same ``residual`` / ``history`` fields.  The raise sites get
+    subclasses of both classes (still subclasses of this package's own, so
+    ``except paper_1906_04572_b200.CorutvError`` keeps working).
+    Idempotent; False if the reference module lacks the classes."""
+    import sys
+
+    from . import _lib, errors as ours, rpca as _rpca
+
+    ref_base = getattr(errs, "CorutvError", None)
+    ref_conv = getattr(errs, "ConvergenceError", None)
+    if ref_base is None or ref_conv is None:
+        return False
+    if issubclass(_lib.ConvergenceError, ref_conv) and issubclass(_lib.CorutvError, ref_base):
+        return True
+    base = type("CorutvError", (ours.CorutvError, ref_base), {"__module__": ours.__name__})
+    conv = type("ConvergenceError", (ours.ConvergenceError, ref_conv), {"__module__": ours.__name__})
+    for mod in (_lib, _rpca, sys.modules[__name__]):
+        if hasattr(mod, "CorutvError"):
+            mod.CorutvError = base
+        if hasattr(mod, "ConvergenceError"):
+            mod.ConvergenceError = conv
+    return True
+
+
 def install(ref_pkg=None):
     """Rebind the reference package's hot-path entry points to the device
     implementation (the binding a maintainer adds).
@@ -73,6 +102,12 @@ def install(ref_pkg=None):
         if hasattr(mod, name):
             setattr(mod, name, obj)
             done.append(f"{mod.__name__}.{name}")
+    try:
+        errs = importlib.import_module(f"{ref_pkg.__name__}.errors")
+    except ImportError:
+        errs = None
+    if errs is not None and _adopt_reference_errors(errs):
+        done.append(f"{errs.__name__}.CorutvError/ConvergenceError (base classes)")
     for name, obj in (("corutv", corutv), ("alm_corutv", alm_corutv)):
         setattr(ref_pkg, name, obj)
         done.append(f"{ref_pkg.__name__}.{name}")

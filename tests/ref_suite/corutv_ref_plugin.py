@@ -51,6 +51,8 @@ def pytest_configure(config):
 
     done = P.install(ref)
     for full in done:
+        if not full.replace(".", "").replace("_", "").isalnum():
+            continue  # e.g. the exception base-class adoption note
         modname, name = full.rsplit(".", 1)
         mod = sys.modules[modname]
         setattr(mod, name, _counted(full, getattr(mod, name)))

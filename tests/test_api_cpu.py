@@ -133,6 +133,12 @@ def test_install_rebinds_the_real_reference_package():
         "assert corutv.rpca.alm_corutv is P.alm_corutv and corutv.rpca.inexact_alm is P.inexact_alm\n"
         "assert corutv.sketch.sor_svd is P.sor_svd and corutv.sketch.tsr_svd is P.tsr_svd\n"
         "from corutv.sketch import corutv as c; assert c is P.corutv\n"
+        "import corutv.errors as E\n"
+        "assert issubclass(P.ConvergenceError, E.ConvergenceError) and issubclass(P.CorutvError, E.CorutvError)\n"
+        "import paper_1906_04572_b200.errors as OE; assert issubclass(P.ConvergenceError, OE.ConvergenceError)\n"
+        "try:\n    raise P.ConvergenceError('cap', residual=1.0, history=[1, 2])\n"
+        "except E.ConvergenceError as e:\n    assert e.history == [1, 2] and e.residual == 1.0\n"
+        "P.install(corutv)\n"
         "print(len(done))\n" % (str(ROOT), str(ref), str(ref)))
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stderr
