@@ -25,6 +25,7 @@
 #include "aux.cuh"
 #include "common.cuh"
 #include "gemm.cuh"
+#include "qrcp_reg.cuh"
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
@@ -34,6 +35,7 @@
 #include "qrcp_cluster.cuh"
 #include "qrcp_grid.cuh"
 #include "small.cuh"
+#include "chol_reg.cuh"
 #include "jacobi_grid.cuh"
 #include "skinny.cuh"
 #include "snorm.cuh"
@@ -618,6 +620,7 @@ struct QrWork {
   double* gwork;  // ell * ell
   double* ws;     // split-K scratch (shared: stream-ordered)
   small::CholInfo* info;  // device
+  int* qd = nullptr;      // device {plain, done, status, steps}: speculative schedule (optional)
 };
 
 struct QrJob {
@@ -644,6 +647,7 @@ void cholqr_multi(corutv_handle* h, QrJob* jobs, int njobs, int ell, int64_t ldx
   // updates) wins from l ~ 64 on (C2 l = 50: equal, C3 l = 110: -0.8 ms/step)
   static const bool force_cluster = std::getenv("CORUTV_CHOL_CLUSTER") != nullptr;  // tuning knob
   const bool smem = aug + static_smem <= (size_t)optin && l < 64 && !force_cluster;
+  static const bool chol_legacy = std::getenv("CORUTV_CHOL_LEGACY") != nullptr;  // A/B knob
   // the cluster kernel stages each 32-row panel in shared memory up to
   // l ~ 840; larger cores read the panel from L2 (GSTAGE)
   const bool gstage = (size_t)chc::smem_doubles(l) * 8 > (size_t)optin;
@@ -656,7 +660,27 @@ void cholqr_multi(corutv_handle* h, QrJob* jobs, int njobs, int ell, int64_t ldx
     set_smem(h, cl_kern, cl_smem);
     if (cl_cs > 8) CK(cudaFuncSetAttribute(cl_kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   }
+  // speculative schedule: with the register factor kernel the step rule
+  // runs on the device (a finished job's further steps are exact no-ops,
+  // R^-1 = I), so the first kSpecSteps steps of every job are queued with no
+  // host sync and their outcome is read once.  Only for sketches small
+  // enough that a wasted no-op step costs less than a sync.
+  constexpr int kSpecSteps = 3;
+  bool spec = smem && !chol_legacy && l <= 32;
+  for (int j = 0; j < njobs; ++j)
+    spec = spec && jobs[j].w.qd && !jobs[j].done && (!jobs[j].sharded || h->nccl) &&
+           (double)jobs[j].rows * l * 8 <= 48.0 * (1 << 20);
+  bool spec_now = false;  // steps currently launched carry the device state
   auto launch_factor = [&](QrJob& q, double coeff) {
+    if (smem && !chol_legacy && l <= 32) {
+      // register kernel for l <= 32 (it also keeps the step rule on the
+      // device for the speculative schedule); above, the shared-memory
+      // kernel is faster (C2 l = 50: 40 vs 63 us)
+      int* qd = spec_now ? q.w.qd : nullptr;
+      creg::chol_reg_kernel<32, 2><<<1, 128, 0, h->stream>>>(q.w.G, l, ldx, coeff, 1, kKappaPlain, q.w.rinvT, ldx, q.w.info, qd);
+      CK_LAUNCH();
+      return;
+    }
     if (smem) {
       small::chol_factor_kernel<<<1, 512, aug, h->stream>>>(q.w.G, l, ldx, coeff, 1, kKappaPlain, q.w.rinvT,
                                                           ldx, q.w.gwork, 1, q.w.info);
@@ -699,7 +723,49 @@ void cholqr_multi(corutv_handle* h, QrJob* jobs, int njobs, int ell, int64_t ldx
     CK(cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&h->join_ev, cudaEventDisableTiming));
   }
-  for (int step = 0; step < kMaxQrSteps; ++step) {
+  int step0 = 0;
+  if (spec) {
+    for (int j = 0; j < njobs; ++j) CK(cudaMemsetAsync(jobs[j].w.qd, 0, 4 * sizeof(int), h->stream));
+    spec_now = true;
+    for (int step = 0; step < kSpecSteps; ++step) {
+      if (pair) {
+        CK(cudaEventRecord(h->fork_ev, h->stream));
+        CK(cudaStreamWaitEvent(h->side, h->fork_ev, 0));
+        struct StreamSwap {
+          corutv_handle* h;
+          cudaStream_t saved;
+          ~StreamSwap() { h->stream = saved; }
+        } swap{h, h->stream};
+        h->stream = h->side;
+        run_step(jobs[1], 1);
+        CK(cudaEventRecord(h->join_ev, h->side));
+        h->stream = swap.saved;
+        run_step(jobs[0], 0);
+        CK(cudaStreamWaitEvent(h->stream, h->join_ev, 0));
+      } else {
+        for (int j = 0; j < njobs; ++j) run_step(jobs[j], j);
+      }
+    }
+    spec_now = false;
+    for (int j = 0; j < njobs; ++j)
+      CK(cudaMemcpyAsync(reinterpret_cast<int*>(h->pinned + 32) + 4 * j, jobs[j].w.qd, 4 * sizeof(int),
+                         cudaMemcpyDeviceToHost, h->stream));
+    if (extra_flag)
+      CK(cudaMemcpyAsync(h->pinned + 60, extra_flag, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    sync(h);
+    if (extra_flag && h->pinned[60] != 0.0) fail(h, CORUTV_ERR_NONFINITE, "a contains non-finite entries");
+    extra_flag = nullptr;
+    for (int j = 0; j < njobs; ++j) {
+      const int* qd = reinterpret_cast<const int*>(h->pinned + 32) + 4 * j;
+      QrJob& q = jobs[j];
+      q.steps = qd[3];
+      if (qd[2] == 2) fail(h, CORUTV_ERR_NONFINITE, "sketch contains non-finite entries");
+      q.plain = qd[0];
+      q.done = qd[1] != 0;
+    }
+    step0 = kSpecSteps;
+  }
+  for (int step = step0; step < kMaxQrSteps; ++step) {
     int active = 0;
     for (int j = 0; j < njobs; ++j) active += jobs[j].done ? 0 : 1;
     if (!active) return;
@@ -721,11 +787,11 @@ void cholqr_multi(corutv_handle* h, QrJob* jobs, int njobs, int ell, int64_t ldx
       for (int j = 0; j < njobs; ++j)
         if (!jobs[j].done) run_step(jobs[j], j);
     }
-    if (step == 0 && extra_flag)
+    if (extra_flag)
       CK(cudaMemcpyAsync(h->pinned + 60, extra_flag, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     sync(h);
-    if (step == 0 && extra_flag && h->pinned[60] != 0.0)
-      fail(h, CORUTV_ERR_NONFINITE, "a contains non-finite entries");
+    if (extra_flag && h->pinned[60] != 0.0) fail(h, CORUTV_ERR_NONFINITE, "a contains non-finite entries");
+    extra_flag = nullptr;
     for (int j = 0; j < njobs; ++j) {
       QrJob& q = jobs[j];
       if (q.done) continue;
@@ -809,6 +875,17 @@ void qrcp(corutv_handle* h, const double* D, int l, int64_t ldd, double* T, int6
           int64_t ldq, long long* perm_out, int* perm32, double* gwork, double delta = -1.0,
           int* r_dev = nullptr) {
   const int optin = max_optin_smem(h);
+  // narrow cores: register-resident QRCP (qrcp_reg.cuh), one barrier a step
+  static const bool reg_off = std::getenv("CORUTV_QRCP_LEGACY") != nullptr;  // A/B knob
+  if (l <= 64 && !reg_off) {
+    // 4 threads per column: measured against 1 (64-long dependent DFMA
+    // chains, 4x slower) and the smem kernel (C1 l = 15: 25 vs 43 us; C2
+    // l = 50: 111 vs 144 us)
+    if (l <= 32) qreg::qrcp_reg_kernel<32, 4><<<1, 128, 0, h->stream>>>(D, l, ldd, T, ldt, qtT, ldq, perm_out, perm32, delta, r_dev);
+    else qreg::qrcp_reg_kernel<64, 4><<<1, 256, 0, h->stream>>>(D, l, ldd, T, ldt, qtT, ldq, perm_out, perm32, delta, r_dev);
+    CK_LAUNCH();
+    return;
+  }
   // small cores: one CTA with R and Q in shared memory, ~G*l threads
   const size_t one = (size_t)l * l * 8;
   const size_t stat128 = 5 * 128 * 8 + 4 * 128 * 4 + 1024;
@@ -1380,12 +1457,14 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   jobs[0].rows_global = mg;
   jobs[0].sharded = sharded;
   jobs[0].w = QrWork{G, rinvT, gwork, ws, info};
+  jobs[0].w.qd = reinterpret_cast<int*>(info + 1);
   jobs[1].cur = c2;
   jobs[1].nxt = C2a;
   jobs[1].rows = n;
   jobs[1].rows_global = (double)n;
   jobs[1].sharded = false;
   jobs[1].w = QrWork{G2, rinvT2, gwork2, ws_qr2 ? ws_qr2 : ws, info + 2};
+  jobs[1].w.qd = reinterpret_cast<int*>(info + 3);
   cholqr_multi(h, jobs, 2, l, ldp, flagd);
   double* Q1 = jobs[0].cur;
   double* Q2 = jobs[1].cur;
@@ -1547,12 +1626,14 @@ void tsr(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, i
   jobs[0].rows_global = (double)m;
   jobs[0].sharded = false;
   jobs[0].w = QrWork{G, rinvT, gwork, ws, info};
+  jobs[0].w.qd = reinterpret_cast<int*>(info + 1);
   jobs[1].cur = Z;
   jobs[1].nxt = Zb;
   jobs[1].rows = n;
   jobs[1].rows_global = (double)n;
   jobs[1].sharded = false;
   jobs[1].w = QrWork{G2, rinvT2, gwork2, ws, info + 2};
+  jobs[1].w.qd = reinterpret_cast<int*>(info + 3);
   cholqr_multi(h, jobs, 2, l, ldp, flagd);
   const double* Q1 = jobs[0].cur;
   const double* Q2 = jobs[1].cur;
@@ -1641,11 +1722,12 @@ void lowrank_op(corutv_handle* h, int mode, const double* u, const double* t, co
     auto al = [](const void* q) { return q == nullptr || (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
     p.vec = ((p.ld & 1) == 0) && al(p.m_mat) && al(p.s) && al(p.y) && al(p.g_next);
   }
+  const int nparts = grid;
   if (mode == gemm::LR_STORE) launch_lr<gemm::LR_STORE>(h, J, mu, mw, tl, p, grid);
   else if (mode == gemm::LR_ALM) launch_lr<gemm::LR_ALM>(h, J, mu, mw, tl, p, grid);
   else launch_lr<gemm::LR_RESID>(h, J, mu, mw, tl, p, grid);
   if (mode != gemm::LR_STORE) {
-    aux::finalize_sums_kernel<<<1, 1024, 0, h->stream>>>(part, mode == gemm::LR_ALM ? cnt : nullptr, grid, out);
+    aux::finalize_sums_kernel<<<1, 1024, 0, h->stream>>>(part, mode == gemm::LR_ALM ? cnt : nullptr, nparts, out);
     CK_LAUNCH();
     if (is_sharded(h)) allreduce(h, out, 2);
     CK(cudaMemcpyAsync(h->pinned, out, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
