@@ -291,7 +291,41 @@ void set_smem(corutv_handle* h, K kern, size_t bytes) {
 struct GemmPlan {
   int J, n_tiles, m_tiles, k_tiles, splits, kps;
   int WN = 2;  // warps along N: 2 -> CTA 128 x 16J; 1 -> CTA 256 x 8J (N <= 64)
+  int sk_grid = 0;  // > 0: stream-K over this many CTAs, `splits` = slots per tile
 };
+
+// Stream-K plan (gemm::sk_cta_of): a persistent grid of min(SMs, units)
+// CTAs, each a contiguous run of (tile, k-tile) units; returns the number of
+// partial slots a tile needs (the most CTAs any tile is split across).
+int sk_slots(int64_t tiles, int64_t k_tiles, int G) {
+  const long long U = (long long)tiles * k_tiles;
+  int smax = 1;
+  for (int64_t t = 0; t < tiles; ++t) {
+    const int c0 = gemm::sk_cta_of(t * k_tiles, U, G);
+    const int c1 = gemm::sk_cta_of((t + 1) * k_tiles - 1, U, G);
+    smax = std::max(smax, c1 - c0 + 1);
+  }
+  return smax;
+}
+
+// Turn a split-K plan into a stream-K one when the classic grid would leave
+// SMs idle in its last wave (the spectral norm's N = 24 sweeps: 440 CTAs in
+// 2.97 waves); only for consumers of the partial slots.
+void make_stream_k(const corutv_handle* h, GemmPlan& p) {
+  // opt-in (A/B knob): measured no faster than the classic 3-wave split-K
+  // grid on the spectral norm's sweeps (153.8 vs 152.8 ms for 352 iterations)
+  static const bool off = std::getenv("CORUTV_STREAMK") == nullptr;
+  const int64_t tiles = (int64_t)p.m_tiles * p.n_tiles;
+  const long long U = (long long)tiles * p.k_tiles;
+  if (off || p.k_tiles < 8 || U < 2LL * h->num_sms) return;
+  // one SM left free: the spectral norm's lambda_max kernel runs beside the
+  // z = A' w sweep on the side stream, and a persistent grid that needs
+  // every SM would wait for it (measured: +65 us a sweep)
+  const int G = h->num_sms - 1;
+  const int slots = sk_slots(tiles, p.k_tiles, G);
+  p.sk_grid = G;
+  p.splits = slots;
+}
 
 GemmPlan plan_gemm(const corutv_handle* h, int64_t M, int64_t N, int64_t K, bool allow_split) {
   GemmPlan p;
@@ -324,7 +358,12 @@ GemmPlan plan_gemm(const corutv_handle* h, int64_t M, int64_t N, int64_t K, bool
   p.m_tiles = (int)((M + bm - 1) / bm);
   p.k_tiles = (int)((K + gemm::BK - 1) / gemm::BK);
   const int64_t base = (int64_t)p.m_tiles * p.n_tiles;
-  const int sms = h->num_sms;
+  // CTA slots per wave: two per SM for the narrow tiles (launch_gemm_t)
+  static const bool one_cta = [] {
+    const char* e = std::getenv("CORUTV_GEMM_MINB");
+    return e && std::atoi(e) == 1;
+  }();
+  const int sms = h->num_sms * ((p.WN == 1 && p.J <= 4 && !one_cta) ? 2 : 1);
   int best = 1;
   double best_cost = 1e300;
   const int smax = allow_split ? std::min(2 * sms, std::max(1, p.k_tiles / 4)) : 1;
@@ -345,14 +384,31 @@ GemmPlan plan_gemm(const corutv_handle* h, int64_t M, int64_t N, int64_t K, bool
   return p;
 }
 
+template <int J, bool MM, bool CHECK, int WN, int MINB>
+void launch_gemm_b(corutv_handle* h, const CUtensorMap& ma, const CUtensorMap& mb, const gemm::Tile& t,
+                   const gemm::StoreParams& sp, int grid) {
+  auto kern = gemm::gemm_kernel<J, MM, CHECK, WN, MINB>;
+  set_smem(h, kern, gemm::smem_bytes(J, WN, MINB));
+  ProfScope ps(h, h->tag, 2.0 * t.M * t.N * (double)t.K);
+  kern<<<grid, gemm::THREADS, gemm::smem_bytes(J, WN, MINB), h->stream>>>(ma, mb, t, sp);
+  CK_LAUNCH();
+}
+
 template <int J, bool MM, bool CHECK, int WN>
 void launch_gemm_t(corutv_handle* h, const CUtensorMap& ma, const CUtensorMap& mb, const gemm::Tile& t,
                    const gemm::StoreParams& sp, int grid) {
-  auto kern = gemm::gemm_kernel<J, MM, CHECK, WN>;
-  set_smem(h, kern, gemm::smem_bytes(J, WN));
-  ProfScope ps(h, h->tag, 2.0 * t.M * t.N * (double)t.K);
-  kern<<<grid, gemm::THREADS, gemm::smem_bytes(J, WN), h->stream>>>(ma, mb, t, sp);
-  CK_LAUNCH();
+  // narrow tiles (256 x 8J, J <= 4): two CTAs per SM
+  static const int two = [] {
+    const char* e = std::getenv("CORUTV_GEMM_MINB");  // A/B knob: 1 forces one CTA per SM
+    return e ? std::atoi(e) : 2;
+  }();
+  if constexpr (WN == 1 && J <= 4) {
+    if (two == 2) {
+      launch_gemm_b<J, MM, CHECK, WN, 2>(h, ma, mb, t, sp, grid);
+      return;
+    }
+  }
+  launch_gemm_b<J, MM, CHECK, WN, 1>(h, ma, mb, t, sp, grid);
 }
 
 template <bool MM, bool CHECK, int WN>
@@ -393,7 +449,10 @@ void zero2d(corutv_handle* h, double* p, int64_t rows, int64_t cols, int64_t ld)
 size_t gemm_ws_elems(const corutv_handle* h, int64_t M, int64_t N, int64_t K) {
   GemmPlan p = plan_gemm(h, M, N, K, true);
   const int64_t ldw = round_up(N, 2);
-  return (size_t)(p.splits > 1 ? p.splits * M * ldw : 0) + (size_t)M * ldw /* transposed path */;
+  GemmPlan q = p;
+  make_stream_k(h, q);
+  const int64_t slots = std::max(p.splits, q.splits);
+  return (size_t)(slots > 1 ? slots * M * ldw : 0) + (size_t)M * ldw /* transposed path */;
 }
 
 // mm == false: C = A (M x K, lda) * Bt^T, Bt: N x K (ldb)
@@ -429,6 +488,14 @@ void run_gemm(corutv_handle* h, bool mm, int64_t M, int64_t N, int64_t K, const 
   t.k_tiles = p.k_tiles;
   t.k_tiles_per_split = p.kps;
   t.splits = p.splits;
+  t.sk = 0;
+  if (partials && !force) {
+    make_stream_k(h, p);
+    if (p.sk_grid > 0) {
+      t.sk = p.splits;
+      t.splits = p.splits;
+    }
+  }
   CUtensorMap ma, mb;
   t.mm3d = 0;
   if (!mm) {
@@ -449,9 +516,9 @@ void run_gemm(corutv_handle* h, bool mm, int64_t M, int64_t N, int64_t K, const 
   if (l2_hint && p.n_tiles == 1 && (double)M * (double)K * 8.0 > 256.0 * (1 << 20)) t.mm3d |= 4;
   static const bool debug_plan = std::getenv("CORUTV_DEBUG_PLAN") != nullptr;
   if (debug_plan)
-    std::fprintf(stderr, "[corutv] gemm %s M=%lld N=%lld K=%lld J=%d WN=%d tiles=%dx%d splits=%d kps=%d mm3d=%d\n",
+    std::fprintf(stderr, "[corutv] gemm %s M=%lld N=%lld K=%lld J=%d WN=%d tiles=%dx%d splits=%d kps=%d mm3d=%d sk=%d\n",
                  mm ? "MM" : "KK", (long long)M, (long long)N, (long long)K, p.J, p.WN, p.m_tiles, p.n_tiles, p.splits,
-                 p.kps, t.mm3d);
+                 p.kps, t.mm3d, p.sk_grid);
   if (partials) *partials = p;
   const bool direct = !partials && (p.splits == 1 && Ct == nullptr && C != nullptr);
   const int64_t ldw = round_up(N, 2);
@@ -466,7 +533,7 @@ void run_gemm(corutv_handle* h, bool mm, int64_t M, int64_t N, int64_t K, const 
     sp.ldc = ldw;
     sp.split_stride = M * ldw;
   }
-  const int grid = p.m_tiles * p.n_tiles * p.splits;
+  const int grid = p.sk_grid > 0 ? p.sk_grid : p.m_tiles * p.n_tiles * p.splits;
   if (mm) {
     if (bad_flag) launch_gemm_j<true, true>(h, p.J, p.WN, ma, mb, t, sp, grid);
     else launch_gemm_j<true, false>(h, p.J, p.WN, ma, mb, t, sp, grid);
@@ -1697,6 +1764,7 @@ void lowrank_op(corutv_handle* h, int mode, const double* u, const double* t, co
   ar.commit();
   gemm::Tile tl;
   tl.mm3d = 0;
+  tl.sk = 0;
   tl.M = (int)rows;
   tl.N = (int)cols;
   tl.K = r;

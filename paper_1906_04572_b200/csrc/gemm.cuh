@@ -40,11 +40,16 @@ __host__ __device__ constexpr int stage_bytes(int J, int WN = 2) { return a_stag
 __host__ __device__ constexpr int stage_tx(int J, int WN, bool MM) {
   return a_stage_bytes(WN) + (MM ? b_stage_bytes(J, WN) : bn_of(J, WN) * BK * 8);
 }
-__host__ __device__ constexpr int num_stages(int J, int WN = 2) {
-  return (SMEM_BUDGET - 1024) / stage_bytes(J, WN) > 8 ? 8 : (SMEM_BUDGET - 1024) / stage_bytes(J, WN);
+// MINB = CTAs per SM the launch targets: 2 halves the ring (112 KB each)
+// so two CTAs -- twice the independent DMMA accumulator chains per SM
+// sub-partition -- share an SM (narrow-N sweeps, whose 12 chains per warp
+// leave the DMMA pipe latency-bound at one CTA per SM)
+__host__ __device__ constexpr int smem_budget(int MINB) { return MINB == 1 ? SMEM_BUDGET : 112 * 1024; }
+__host__ __device__ constexpr int num_stages(int J, int WN = 2, int MINB = 1) {
+  return (smem_budget(MINB) - 1024) / stage_bytes(J, WN) > 8 ? 8 : (smem_budget(MINB) - 1024) / stage_bytes(J, WN);
 }
-__host__ __device__ constexpr int smem_bytes(int J, int WN = 2) {
-  return 1024 /*align slack*/ + num_stages(J, WN) * stage_bytes(J, WN) + 2 * 8 * 8 + 64;
+__host__ __device__ constexpr int smem_bytes(int J, int WN = 2, int MINB = 1) {
+  return 1024 /*align slack*/ + num_stages(J, WN, MINB) * stage_bytes(J, WN) + 2 * 8 * 8 + 64;
 }
 // low-rank (ALM / residual / store) kernels: K = r is short, so 2 stages; the
 // same bytes are reused to stage the 128 x (16J + 2) result tile.
@@ -63,7 +68,20 @@ struct Tile {
   int splits;
   int mm3d;             // MM operands as one 3-D box per stage: bit 0 A, bit 1 B;
                         // bit 2: A (the data matrix, read once) loaded evict-first
+  int sk;               // > 0: stream-K (persistent grid over the linear (tile, k-tile)
+                        // space; sk = partial slots per tile), 0: classic split-K
 };
+
+// Stream-K partition: CTA c of G owns units [c U / G, (c + 1) U / G) of the
+// U = tiles * k_tiles linear (tile, k-tile) space; sk_cta_of(u) is the CTA
+// owning unit u.  A tile's partial slots are numbered by owning CTA in
+// order, so the finalize sums them in a fixed order (deterministic).
+__host__ __device__ inline int sk_cta_of(long long u, long long U, int G) {
+  int c = (int)((u * G) / U);
+  while (c + 1 < G && ((long long)(c + 1) * U) / G <= u) ++c;
+  while (c > 0 && ((long long)c * U) / G > u) --c;
+  return c;
+}
 
 // Accumulator for one consumer warp: 4 (M) x J (N) DMMA fragments.
 template <int J>
@@ -156,15 +174,23 @@ template <int J, bool MM, bool CHECK, int S = num_stages(J), int WN = 2>
 __device__ __forceinline__ void mainloop(const Smem& sm, const CUtensorMap* mapA,
                                          const CUtensorMap* mapB, int m0, int n0, int kt0,
                                          int kt1, Acc<J>& acc, int wm, int wn, int lane, int nvf,
-                                         int mvf, bool& bad, int mm3d = 0) {
+                                         int mvf, bool& bad, int mm3d = 0, int i0 = 0) {
+  // i0: ring iterations already run by this CTA (stream-K: a second
+  // segment continues the ring where the first left it)
   (void)nvf;
   (void)mvf;
   const int nkt = kt1 - kt0;
   const bool leader = threadIdx.x == 0;
   if (leader) {
-    tma_prefetch_desc(mapA);
-    tma_prefetch_desc(mapB);
-    for (int i = 0; i < S && i < nkt; ++i) issue_stage<J, MM, WN>(sm, mapA, mapB, m0, n0, kt0 + i, i, mm3d);
+    if (i0 == 0) {
+      tma_prefetch_desc(mapA);
+      tma_prefetch_desc(mapB);
+    }
+    for (int i = 0; i < S && i < nkt; ++i) {
+      const int g = i0 + i;
+      if (g >= S) mbar_wait(&sm.empty[g % S], ((g / S) - 1) & 1);
+      issue_stage<J, MM, WN>(sm, mapA, mapB, m0, n0, kt0 + i, g % S, mm3d);
+    }
   }
   const int r8 = lane >> 2, c4 = lane & 3;
   // per-lane element offsets (in doubles) inside one stage
@@ -184,11 +210,12 @@ __device__ __forceinline__ void mainloop(const Smem& sm, const CUtensorMap* mapA
     for (int s = 0; s < 4; ++s) mmB[s] = (s + 4 * c4) * 16;
   }
   for (int i = 0; i < nkt; ++i) {
-    const int st = i % S;
-    const uint32_t ph = (i / S) & 1;
+    const int st = (i0 + i) % S;
+    const uint32_t ph = ((i0 + i) / S) & 1;
     if (leader && i >= 1 && (i - 1) + S < nkt) {
-      const int ps = (i - 1) % S;
-      mbar_wait(&sm.empty[ps], ((i - 1) / S) & 1);
+      const int g = i0 + i - 1;
+      const int ps = g % S;
+      mbar_wait(&sm.empty[ps], (g / S) & 1);
       issue_stage<J, MM, WN>(sm, mapA, mapB, m0, n0, kt0 + (i - 1) + S, ps, mm3d);
     }
     mbar_wait(&sm.full[st], ph);
@@ -282,43 +309,17 @@ struct StoreParams {
   int* bad_flag;         // nullable: set to 1 if a non-finite A entry was read
 };
 
-template <int J, bool MM, bool CHECK, int WN = 2>
-__global__ void __launch_bounds__(THREADS, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                Tile t, StoreParams sp) {
-  extern __shared__ unsigned char smem_raw[];
-  constexpr int S = num_stages(J, WN);
-  Smem sm = carve<J, S, S * stage_bytes(J, WN), WN>(smem_raw);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int bid = blockIdx.x;
-  const int nt = bid % t.n_tiles;
-  const int rest = bid / t.n_tiles;
-  const int m0 = (rest % t.m_tiles) * bm_of(WN);
-  const int split = rest / t.m_tiles;
-  const int n0 = nt * bn_of(J, WN);
-  const int kt0 = split * t.k_tiles_per_split;
-  const int kt1 = min(t.k_tiles, kt0 + t.k_tiles_per_split);
-  init_barriers<S>(sm);
-  constexpr int WMW = NCW / WN;  // warps along M
-  const int wm = warp % WMW, wn = warp / WMW;
-  const int ncol0 = n0 + wn * 8 * J;
-  const int nvf = max(0, min(J, (t.N - ncol0 + 7) / 8));
-  const int mvf = max(0, min(4, (t.M - (m0 + wm * 32) + 7) / 8));
-  Acc<J> acc;
-  acc.zero();
-  bool bad = false;
-  mainloop<J, MM, CHECK, S, WN>(sm, &mapA, &mapB, m0, n0, kt0, kt1, acc, wm, wn, lane, nvf, mvf, bad, t.mm3d);
-  if (CHECK && sp.bad_flag) {
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(sp.bad_flag, 1);
-  }
-  double* out = sp.c + (int64_t)split * sp.split_stride;
-  const bool vec = ((sp.ldc & 1) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+// Store one warp's accumulator tile (rows m0.., columns ncol0..) to out.
+template <int J, bool MM>
+__device__ __forceinline__ void store_acc(const Acc<J>& acc, double* out, int64_t ldc, const Tile& t, int m0,
+                                          int ncol0, int wm, int lane) {
+  const bool vec = ((ldc & 1) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
   const int r8 = lane >> 2, c4 = lane & 3;
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi) {
     const int row = MM ? m0 + wm * 32 + 16 * (mi >> 1) + 2 * r8 + (mi & 1) : m0 + wm * 32 + mi * 8 + r8;
     if (row >= t.M) continue;
-    double* rowp = out + (int64_t)row * sp.ldc;
+    double* rowp = out + (int64_t)row * ldc;
 #pragma unroll
     for (int nj = 0; nj < J; ++nj) {
       if (MM && nj < (J & ~1)) {
@@ -342,6 +343,78 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   }
+}
+
+template <int J, bool MM, bool CHECK, int WN = 2, int MINB = 1>
+__global__ void __launch_bounds__(THREADS, MINB)
+    gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                Tile t, StoreParams sp) {
+  extern __shared__ unsigned char smem_raw[];
+  constexpr int S = num_stages(J, WN, MINB);
+  Smem sm = carve<J, S, S * stage_bytes(J, WN), WN>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int WMW = NCW / WN;  // warps along M
+  const int wm = warp % WMW, wn = warp / WMW;
+  init_barriers<S>(sm);
+  if (t.sk > 0) {
+    // stream-K: this CTA's contiguous run of (tile, k-tile) units, one
+    // segment per tile it touches, the TMA ring continuing across segments
+    const int G = gridDim.x, c = blockIdx.x;
+    const long long U = (long long)t.m_tiles * t.n_tiles * t.k_tiles;
+    long long u = ((long long)c * U) / G;
+    const long long u1 = ((long long)(c + 1) * U) / G;
+    int i0 = 0;
+    while (u < u1) {
+      const int tile = (int)(u / t.k_tiles);
+      const int kt0 = (int)(u % t.k_tiles);
+      const int kt1 = (int)min((long long)t.k_tiles, kt0 + (u1 - u));
+      const int nt = tile % t.n_tiles;
+      const int m0 = (tile / t.n_tiles) * bm_of(WN);
+      const int n0 = nt * bn_of(J, WN);
+      const int ncol0 = n0 + wn * 8 * J;
+      const int nvf = max(0, min(J, (t.N - ncol0 + 7) / 8));
+      const int mvf = max(0, min(4, (t.M - (m0 + wm * 32) + 7) / 8));
+      const int cfirst = sk_cta_of((long long)tile * t.k_tiles, U, G);
+      Acc<J> acc;
+      acc.zero();
+      bool bad = false;
+      mainloop<J, MM, CHECK, S, WN>(sm, &mapA, &mapB, m0, n0, kt0, kt1, acc, wm, wn, lane, nvf, mvf, bad, t.mm3d, i0);
+      if (CHECK && sp.bad_flag) {
+        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(sp.bad_flag, 1);
+      }
+      store_acc<J, MM>(acc, sp.c + (int64_t)(c - cfirst) * sp.split_stride, sp.ldc, t, m0, ncol0, wm, lane);
+      if (kt1 == t.k_tiles) {
+        // the tile's last segment: zero its unused slots so a finalize of
+        // t.sk slices sums exactly the segments
+        Acc<J> z;
+        z.zero();
+        for (int sl = c - cfirst + 1; sl < t.sk; ++sl)
+          store_acc<J, MM>(z, sp.c + (int64_t)sl * sp.split_stride, sp.ldc, t, m0, ncol0, wm, lane);
+      }
+      i0 += kt1 - kt0;
+      u += kt1 - kt0;
+    }
+    return;
+  }
+  const int bid = blockIdx.x;
+  const int nt = bid % t.n_tiles;
+  const int rest = bid / t.n_tiles;
+  const int m0 = (rest % t.m_tiles) * bm_of(WN);
+  const int split = rest / t.m_tiles;
+  const int n0 = nt * bn_of(J, WN);
+  const int kt0 = split * t.k_tiles_per_split;
+  const int kt1 = min(t.k_tiles, kt0 + t.k_tiles_per_split);
+  const int ncol0 = n0 + wn * 8 * J;
+  const int nvf = max(0, min(J, (t.N - ncol0 + 7) / 8));
+  const int mvf = max(0, min(4, (t.M - (m0 + wm * 32) + 7) / 8));
+  Acc<J> acc;
+  acc.zero();
+  bool bad = false;
+  mainloop<J, MM, CHECK, S, WN>(sm, &mapA, &mapB, m0, n0, kt0, kt1, acc, wm, wn, lane, nvf, mvf, bad, t.mm3d);
+  if (CHECK && sp.bad_flag) {
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(sp.bad_flag, 1);
+  }
+  store_acc<J, MM>(acc, sp.c + (int64_t)split * sp.split_stride, sp.ldc, t, m0, ncol0, wm, lane);
 }
 
 // ------------------------------------------------ low-rank product epilogues
