@@ -82,7 +82,10 @@ __device__ bool cta_chol_aug(const double* Gs, int ldg, int b, double shift, dou
     w[q] = g;
   }
   bool bad = false;
-  for (int j = 0; j < B; ++j) {
+  // the padding (rows / columns b..31) is the identity and stays so: the
+  // elimination stops after column b - 1 (b = 24 saves a quarter of the
+  // serial chain)
+  for (int j = 0; j < b; ++j) {
     if (i == j && (j >> 3) == (tid & 7)) {
 #pragma unroll
       for (int q = 0; q < 8; ++q)
@@ -303,12 +306,16 @@ __device__ __forceinline__ void upper_ij(int u, int b, int* i, int* j) {
   *j = r + rem;
 }
 
-__device__ bool last_cta_reduce(const double* part, double* part2, int b, unsigned* tickets, double* Gs) {
+// slot / count: this contributor's slot and the number of slots (the CTA
+// index and grid size for the row kernels; the tile index and tile count
+// for the fused sweep epilogue of gemm_snorm_kernel).
+__device__ bool last_cta_reduce(const double* part, double* part2, int b, unsigned* tickets, double* Gs, int slot,
+                                int count) {
   __shared__ int am_last;
   constexpr int bb = B * B;
   const int nu = b * (b + 1) / 2;
-  const int group = blockIdx.x / GS, ngroups = (gridDim.x + GS - 1) / GS;
-  const int gsize = min(GS, (int)gridDim.x - group * GS);
+  const int group = slot / GS, ngroups = (count + GS - 1) / GS;
+  const int gsize = min(GS, count - group * GS);
   int idx[UMAX];
 #pragma unroll
   for (int q = 0; q < UMAX; ++q) {
@@ -418,14 +425,14 @@ __device__ __forceinline__ void gram_chunk(const double* x, int nr4, double (&ac
   }
 }
 
-__device__ __forceinline__ void gram_store(const double (&acc)[2][2], double* part) {
+__device__ __forceinline__ void gram_store(const double (&acc)[2][2], double* part, int idx) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r8 = lane >> 2, c4 = lane & 3;
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
     const int q = 2 * warp + t, bi = q >> 2, bj = q & 3;
 #pragma unroll
-    for (int e = 0; e < 2; ++e) part[(int64_t)blockIdx.x * B * B + (bi * 8 + r8) * B + bj * 8 + 2 * c4 + e] = acc[t][e];
+    for (int e = 0; e < 2; ++e) part[(int64_t)idx * B * B + (bi * 8 + r8) * B + bj * 8 + 2 * c4 + e] = acc[t][e];
   }
 }
 
@@ -485,33 +492,18 @@ __device__ __forceinline__ void store_chunk(const double* x, int nr, int b, int6
 // writes the reduced Gram w'w (32 x 32, padded) to lam for lmax_kernel.
 // MODE 1 (z = A' w): finalize z into out (the CholeskyQR buffer) + outT;
 // Gram; the last CTA takes the first factor step into st.
+// Rows [r0, r1) of a finalize: the split-K sum of the nr x b elements in
+// fixed slice order (per thread 4 elements x up to 16 slices of loads in
+// flight before any add), times the pending R^-1 for MODE 0, stored to out
+// (+ outT), and their Gram accumulated into acc.  Ends with a barrier.
 template <int MODE>
-__global__ void __launch_bounds__(THREADS, 1)
-    finalize_kernel(const double* __restrict__ ws, int splits, int64_t sstride, int64_t ldw, int64_t rows, int b,
-                    double* __restrict__ out, int64_t ldo, double* __restrict__ outT, int64_t ldoT,
-                    double* __restrict__ part, double* __restrict__ part2, unsigned* tickets, double* lam,
-                    QrState* st, double shift_coeff, double kappa_max, int use_pending) {
-  __shared__ RowSmem sm;
-  if (MODE == 0) {
-    for (int e = threadIdx.x; e < B * B; e += THREADS)
-      sm.Ri[(e / B) * (B + 1) + e % B] = use_pending ? __ldcg(st->rinv + e) : ((e / B == e % B) ? 1.0 : 0.0);
-  }
-  if (MODE == 1 && blockIdx.x == 0 && threadIdx.x == 0) {
-    // fresh CholeskyQR state (visible to the apply launches after this one)
-    st->plain = 0;
-    st->finish = 0;
-    st->done = 0;
-    st->status = 0;
-    st->steps = 0;
-  }
-  int64_t r0, r1;
-  cta_rows(rows, &r0, &r1);
-  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+__device__ __forceinline__ void finalize_rows(RowSmem& sm, const double* __restrict__ ws, int splits, int64_t sstride,
+                                              int64_t ldw, int64_t r0, int64_t r1, int b, double* __restrict__ out,
+                                              int64_t ldo, double* __restrict__ outT, int64_t ldoT,
+                                              double (&acc)[2][2]) {
   for (int64_t c0 = r0; c0 < r1; c0 += RCH) {
     const int nr = (int)min((int64_t)RCH, r1 - c0), nr4 = (nr + 3) & ~3;
-    // zero the padding (rows nr..nr4, columns b..32), then the split-K sum
-    // of the nr x b elements in fixed order: per thread 4 elements x up to
-    // 16 slices of loads in flight before any add
+    // zero the padding (rows nr..nr4, columns b..32)
     for (int e = threadIdx.x; e < nr4 * B; e += THREADS) {
       const int r = e / B, c = e % B;
       if (r >= nr || c >= b) sm.u.x[r * LDX + c] = 0.0;
@@ -550,8 +542,44 @@ __global__ void __launch_bounds__(THREADS, 1)
     gram_chunk(sm.u.x, nr4, acc);
     __syncthreads();
   }
-  gram_store(acc, part);
-  if (!last_cta_reduce(part, part2, b, tickets, sm.u.f.G)) return;
+}
+
+__device__ __forceinline__ void load_pending_rinv(RowSmem& sm, const QrState* st, int use_pending) {
+  for (int e = threadIdx.x; e < B * B; e += THREADS)
+    sm.Ri[(e / B) * (B + 1) + e % B] = use_pending ? __ldcg(st->rinv + e) : ((e / B == e % B) ? 1.0 : 0.0);
+}
+
+__device__ __forceinline__ void reset_qr_state(QrState* st) {
+  st->plain = 0;
+  st->finish = 0;
+  st->done = 0;
+  st->status = 0;
+  st->steps = 0;
+}
+
+// MODE 0 (w = A v): finalize w from the split-K partials (ws, `splits`
+// slices of stride sstride, ld ldw), times the pending R^-1 of the previous
+// CholeskyQR (its last apply folded in: A (v' R^-1) = (A v') R^-1;
+// identity on the first iteration), into out (+ outT); Gram; the last CTA
+// writes the reduced Gram w'w (32 x 32, padded) to lam for lmax_kernel.
+// MODE 1 (z = A' w): finalize z into out (the CholeskyQR buffer) + outT;
+// Gram; the last CTA takes the first factor step into st.
+template <int MODE>
+__global__ void __launch_bounds__(THREADS, 1)
+    finalize_kernel(const double* __restrict__ ws, int splits, int64_t sstride, int64_t ldw, int64_t rows, int b,
+                    double* __restrict__ out, int64_t ldo, double* __restrict__ outT, int64_t ldoT,
+                    double* __restrict__ part, double* __restrict__ part2, unsigned* tickets, double* lam,
+                    QrState* st, double shift_coeff, double kappa_max, int use_pending) {
+  __shared__ RowSmem sm;
+  if (MODE == 0) load_pending_rinv(sm, st, use_pending);
+  if (MODE == 1 && blockIdx.x == 0 && threadIdx.x == 0) reset_qr_state(st);  // visible to the later applies
+  int64_t r0, r1;
+  cta_rows(rows, &r0, &r1);
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  __syncthreads();
+  finalize_rows<MODE>(sm, ws, splits, sstride, ldw, r0, r1, b, out, ldo, outT, ldoT, acc);
+  gram_store(acc, part, blockIdx.x);
+  if (!last_cta_reduce(part, part2, b, tickets, sm.u.f.G, blockIdx.x, gridDim.x)) return;
   if (MODE == 0) {
     for (int e = threadIdx.x; e < B * B; e += THREADS) lam[e] = sm.u.f.G[e];
   } else {
@@ -612,8 +640,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     gram_chunk(sm.u.x, nr4, acc);
     __syncthreads();
   }
-  gram_store(acc, part);
-  if (!last_cta_reduce(part, part2, b, st->tickets, sm.u.f.G)) return;
+  gram_store(acc, part, blockIdx.x);
+  if (!last_cta_reduce(part, part2, b, st->tickets, sm.u.f.G, blockIdx.x, gridDim.x)) return;
   factor_step(sm.u.f.G, B, b, shift_coeff, kappa_max, st, sm.u.f.W, sm.red, sm.rowj, sm.piv);
   __syncthreads();
   // the launch budget is spent and another step would be needed
