@@ -688,6 +688,7 @@ struct QrWork {
   double* ws;     // split-K scratch (shared: stream-ordered)
   small::CholInfo* info;  // device
   int* qd = nullptr;      // device {plain, done, status, steps}: speculative schedule (optional)
+  sn::QrState* cta_state = nullptr;  // device: whole-QR-in-one-CTA path (optional)
 };
 
 struct QrJob {
@@ -726,6 +727,45 @@ void cholqr_multi(corutv_handle* h, QrJob* jobs, int njobs, int ell, int64_t ldx
   } else {
     set_smem(h, cl_kern, cl_smem);
     if (cl_cs > 8) CK(cudaFuncSetAttribute(cl_kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  }
+  // small sketches (l <= 32, rows resident in L2): the whole CholeskyQR of
+  // every job in ONE launch, one CTA per matrix (snorm.cuh cholqr_cta_kernel),
+  // one host sync for the outcome
+  {
+    static const bool cta_off = std::getenv("CORUTV_CHOLQR_CTA_OFF") != nullptr;  // A/B knob
+    bool ok = !cta_off && l <= 32 && njobs <= 2;
+    for (int j = 0; j < njobs; ++j)
+      ok = ok && jobs[j].w.cta_state && !jobs[j].sharded && !jobs[j].done &&
+           (double)jobs[j].rows * l * 8 <= 6.0 * (1 << 20);
+    if (ok) {
+      sn::CtaJobs cj{};
+      for (int j = 0; j < njobs; ++j) {
+        QrJob& q = jobs[j];
+        cj.j[j] = sn::CtaJob{q.cur, q.nxt, q.rows, ldx, q.w.cta_state,
+                             11.0 * (q.rows_global * l + (double)l * (l + 1)) * kUnit};
+      }
+      sn::cholqr_cta_kernel<<<njobs, sn::THREADS, 0, h->stream>>>(cj, l, kKappaPlain, kMaxQrSteps);
+      CK_LAUNCH();
+      int* outp = reinterpret_cast<int*>(h->pinned + 32);
+      for (int j = 0; j < njobs; ++j) {
+        CK(cudaMemcpyAsync(outp + 4 * j, &jobs[j].w.cta_state->status, sizeof(int), cudaMemcpyDeviceToHost,
+                           h->stream));
+        CK(cudaMemcpyAsync(outp + 4 * j + 1, &jobs[j].w.cta_state->steps, sizeof(int), cudaMemcpyDeviceToHost,
+                           h->stream));
+      }
+      if (extra_flag)
+        CK(cudaMemcpyAsync(h->pinned + 60, extra_flag, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+      sync(h);
+      if (extra_flag && h->pinned[60] != 0.0) fail(h, CORUTV_ERR_NONFINITE, "a contains non-finite entries");
+      for (int j = 0; j < njobs; ++j) {
+        const int status = outp[4 * j];
+        jobs[j].steps = outp[4 * j + 1];
+        if (status == 2) fail(h, CORUTV_ERR_NONFINITE, "sketch contains non-finite entries");
+        if (status == 3) fail(h, CORUTV_ERR_CONVERGENCE, "CholeskyQR did not reach orthogonality");
+        jobs[j].done = true;  // Q in jobs[j].cur
+      }
+      return;
+    }
   }
   // speculative schedule: with the register factor kernel the step rule
   // runs on the device (a finished job's further steps are exact no-ops,
@@ -1439,6 +1479,8 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   ar.add(&perm32, (size_t)ldp);
   ar.add(&jstat, 4);
   ar.add(&info, 4);
+  sn::QrState* cta_st;
+  ar.add((char**)&cta_st, 2 * sizeof(sn::QrState));
   ar.commit();
 
   // host input: start the chunked H2D copy before anything else
@@ -1525,6 +1567,7 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   jobs[0].sharded = sharded;
   jobs[0].w = QrWork{G, rinvT, gwork, ws, info};
   jobs[0].w.qd = reinterpret_cast<int*>(info + 1);
+  jobs[0].w.cta_state = cta_st;
   jobs[1].cur = c2;
   jobs[1].nxt = C2a;
   jobs[1].rows = n;
@@ -1532,6 +1575,7 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   jobs[1].sharded = false;
   jobs[1].w = QrWork{G2, rinvT2, gwork2, ws_qr2 ? ws_qr2 : ws, info + 2};
   jobs[1].w.qd = reinterpret_cast<int*>(info + 3);
+  jobs[1].w.cta_state = cta_st + 1;
   cholqr_multi(h, jobs, 2, l, ldp, flagd);
   double* Q1 = jobs[0].cur;
   double* Q2 = jobs[1].cur;
@@ -1634,6 +1678,8 @@ void tsr(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, i
   ar.add(&flag, 4);
   ar.add(&jstat, 4);
   ar.add(&info, 4);
+  sn::QrState* cta_st;
+  ar.add((char**)&cta_st, 2 * sizeof(sn::QrState));
   // host input: z = A' phi split-K slices as the row chunks land
   const GemmPlan zplan = plan_gemm(h, n, l, m, true);
   double* ws2 = nullptr;
@@ -1694,6 +1740,7 @@ void tsr(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, i
   jobs[0].sharded = false;
   jobs[0].w = QrWork{G, rinvT, gwork, ws, info};
   jobs[0].w.qd = reinterpret_cast<int*>(info + 1);
+  jobs[0].w.cta_state = cta_st;
   jobs[1].cur = Z;
   jobs[1].nxt = Zb;
   jobs[1].rows = n;
@@ -1701,6 +1748,7 @@ void tsr(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, i
   jobs[1].sharded = false;
   jobs[1].w = QrWork{G2, rinvT2, gwork2, ws, info + 2};
   jobs[1].w.qd = reinterpret_cast<int*>(info + 3);
+  jobs[1].w.cta_state = cta_st + 1;
   cholqr_multi(h, jobs, 2, l, ldp, flagd);
   const double* Q1 = jobs[0].cur;
   const double* Q2 = jobs[1].cur;
@@ -1716,10 +1764,10 @@ void tsr(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, i
 }
 
 // --------------------------------------------- low-rank product epilogues
-template <int J, int MODE>
+template <int J, int MODE, int MINB>
 void launch_lr_t(corutv_handle* h, const CUtensorMap& mu, const CUtensorMap& mw, const gemm::Tile& t,
                  const gemm::LrParams& p, int grid) {
-  auto kern = gemm::lowrank_kernel<J, MODE>;
+  auto kern = gemm::lowrank_kernel<J, MODE, MINB>;
   set_smem(h, kern, gemm::lr_smem_bytes(J));
   ProfScope ps(h, 3, 2.0 * t.M * t.N * (double)t.K);
   kern<<<grid, gemm::THREADS, gemm::lr_smem_bytes(J), h->stream>>>(mu, mw, t, p);
@@ -1728,12 +1776,16 @@ void launch_lr_t(corutv_handle* h, const CUtensorMap& mu, const CUtensorMap& mw,
 
 template <int MODE>
 void launch_lr(corutv_handle* h, int J, const CUtensorMap& mu, const CUtensorMap& mw, const gemm::Tile& t,
-               const gemm::LrParams& p, int grid) {
+               const gemm::LrParams& p, int grid, int minb = 2) {
+  if (MODE == gemm::LR_ALM && J == 2 && minb == 3) {
+    launch_lr_t<2, MODE, 3>(h, mu, mw, t, p, grid);
+    return;
+  }
   switch (J) {
-    case 1: launch_lr_t<1, MODE>(h, mu, mw, t, p, grid); break;
-    case 2: launch_lr_t<2, MODE>(h, mu, mw, t, p, grid); break;
-    case 3: launch_lr_t<3, MODE>(h, mu, mw, t, p, grid); break;
-    default: launch_lr_t<4, MODE>(h, mu, mw, t, p, grid); break;
+    case 1: launch_lr_t<1, MODE, 2>(h, mu, mw, t, p, grid); break;
+    case 2: launch_lr_t<2, MODE, 2>(h, mu, mw, t, p, grid); break;
+    case 3: launch_lr_t<3, MODE, 2>(h, mu, mw, t, p, grid); break;
+    default: launch_lr_t<4, MODE, 2>(h, mu, mw, t, p, grid); break;
   }
 }
 
@@ -1746,8 +1798,20 @@ void lowrank_op(corutv_handle* h, int mode, const double* u, const double* t, co
   const int64_t ldr = round_up(std::max(r, 1), 16), ldl = round_up(ell, 16);
   // 128 x 64 tiles (J <= 4): small shared/register footprint -> 2-3 CTAs per
   // SM, so one CTA's TMA mainloop overlaps another's memory-bound epilogue
-  const int n_tiles = (int)((cols + 63) / 64);
-  const int J = (int)std::min<int64_t>(4, std::max<int64_t>(1, (cols + 16 * n_tiles - 1) / (16 * n_tiles)));
+  int n_tiles = (int)((cols + 63) / 64);
+  int J = (int)std::min<int64_t>(4, std::max<int64_t>(1, (cols + 16 * n_tiles - 1) / (16 * n_tiles)));
+  // ALM update: 128 x 32 tiles at three CTAs per SM (A/B knob CORUTV_ALM_J=4
+  // restores round 1's 128 x 64 tiles at two)
+  static const int alm_j = [] {
+    const char* e = std::getenv("CORUTV_ALM_J");
+    return e ? std::atoi(e) : 2;
+  }();
+  int minb = 2;
+  if (mode == gemm::LR_ALM && alm_j == 2 && cols >= 32) {
+    n_tiles = (int)((cols + 31) / 32);
+    J = 2;
+    minb = 3;
+  }
   const int m_tiles = (int)((rows + gemm::BM - 1) / gemm::BM);
   const int grid = m_tiles * n_tiles;
   Arena ar(h);
@@ -1792,7 +1856,7 @@ void lowrank_op(corutv_handle* h, int mode, const double* u, const double* t, co
   }
   const int nparts = grid;
   if (mode == gemm::LR_STORE) launch_lr<gemm::LR_STORE>(h, J, mu, mw, tl, p, grid);
-  else if (mode == gemm::LR_ALM) launch_lr<gemm::LR_ALM>(h, J, mu, mw, tl, p, grid);
+  else if (mode == gemm::LR_ALM) launch_lr<gemm::LR_ALM>(h, J, mu, mw, tl, p, grid, minb);
   else launch_lr<gemm::LR_RESID>(h, J, mu, mw, tl, p, grid);
   if (mode != gemm::LR_STORE) {
     aux::finalize_sums_kernel<<<1, 1024, 0, h->stream>>>(part, mode == gemm::LR_ALM ? cnt : nullptr, nparts, out);

@@ -435,8 +435,11 @@ struct LrParams {
                          // n x n operand 16-byte aligned (checked on the host)
 };
 
-template <int J, int MODE>
-__global__ void __launch_bounds__(THREADS, 2)
+// MINB: CTAs per SM (launch bound).  3 (with J = 2, 128 x 32 tiles and
+// 4 row slots in flight per warp) keeps three CTAs' mainloops and
+// streaming epilogues interleaved on each SM for the rank-r ALM update.
+template <int J, int MODE, int MINB = 2>
+__global__ void __launch_bounds__(THREADS, MINB)
     lowrank_kernel(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapW,
                    Tile t, LrParams p) {
   extern __shared__ unsigned char smem_raw[];
@@ -494,22 +497,29 @@ __global__ void __launch_bounds__(THREADS, 2)
   long long cnt = 0;
   const int ncols = min(TN, t.N - n0);
   const bool vec = p.vec != 0;
-  // Each warp owns rows {4w .. 4w+3} + 32k; a batch of RB rows has all its
-  // M / Y loads issued before any store (Y is read and written, so loads
-  // of later rows could not otherwise move above earlier stores), keeping
-  // RB x 2 x 512 B per warp in flight.  TN <= 64: one double2 per lane.
-  constexpr int RB = 8;
-  const int c = 2 * lane;
+  // Warp w owns rows [16 w, 16 w + 16) of the tile.  LPR lanes cover one
+  // row (2 columns each, double2), RPI = 32 / LPR rows per warp
+  // instruction; RB instruction slots have all their M / Y loads issued
+  // before any store (Y is read and written, so loads of later rows could
+  // not otherwise move above earlier stores): RB x 2 x 512 B per warp in
+  // flight.
+  constexpr int LPR = (TN / 2 <= 16) ? TN / 2 : 32;
+  constexpr int RPI = 32 / LPR;
+  constexpr int RPW = BM / NCW;
+  constexpr int SLOTS = RPW / RPI;
+  constexpr int RB = MINB >= 3 ? 4 : 8;
+  const int lrow = lane / LPR;
+  const int c = 2 * (lane % LPR);
   const bool pair = vec && (c + 1 < ncols);
-  for (int base = warp * 4; base < BM; base += NCW * 4 * (RB / 4)) {
+  for (int s0 = 0; s0 < SLOTS; s0 += RB) {
     double2 mv[RB], yv[RB];
 #pragma unroll
     for (int q = 0; q < RB; ++q) {
-      const int row = base + (q >> 2) * (NCW * 4) + (q & 3);
+      const int row = warp * RPW + (s0 + q) * RPI + lrow;
       const int grow = m0 + row;
       mv[q] = make_double2(0.0, 0.0);
       yv[q] = make_double2(0.0, 0.0);
-      if (MODE != LR_STORE && row < BM && grow < t.M && c < ncols) {
+      if (MODE != LR_STORE && s0 + q < SLOTS && grow < t.M && c < ncols) {
         const int64_t idx = (int64_t)grow * p.ld + n0 + c;
         if (pair) {
           mv[q] = __ldcs(reinterpret_cast<const double2*>(p.m_mat + idx));
@@ -526,9 +536,9 @@ __global__ void __launch_bounds__(THREADS, 2)
     }
 #pragma unroll
     for (int q = 0; q < RB; ++q) {
-      const int row = base + (q >> 2) * (NCW * 4) + (q & 3);
+      const int row = warp * RPW + (s0 + q) * RPI + lrow;
       const int grow = m0 + row;
-      if (row >= BM || grow >= t.M || c >= ncols) continue;
+      if (s0 + q >= SLOTS || grow >= t.M || c >= ncols) continue;
       const int64_t idx = (int64_t)grow * p.ld + n0 + c;
       const double2 l2 = *reinterpret_cast<const double2*>(tileL + row * LDT + c);
       const double lv[2] = {l2.x, l2.y};
