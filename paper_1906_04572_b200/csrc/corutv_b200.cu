@@ -688,7 +688,6 @@ struct QrWork {
   double* ws;     // split-K scratch (shared: stream-ordered)
   small::CholInfo* info;  // device
   int* qd = nullptr;      // device {plain, done, status, steps}: speculative schedule (optional)
-  sn::QrState* cta_state = nullptr;  // device: whole-QR-in-one-CTA path (optional)
 };
 
 struct QrJob {
@@ -727,45 +726,6 @@ void cholqr_multi(corutv_handle* h, QrJob* jobs, int njobs, int ell, int64_t ldx
   } else {
     set_smem(h, cl_kern, cl_smem);
     if (cl_cs > 8) CK(cudaFuncSetAttribute(cl_kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  }
-  // small sketches (l <= 32, rows resident in L2): the whole CholeskyQR of
-  // every job in ONE launch, one CTA per matrix (snorm.cuh cholqr_cta_kernel),
-  // one host sync for the outcome
-  {
-    static const bool cta_off = std::getenv("CORUTV_CHOLQR_CTA_OFF") != nullptr;  // A/B knob
-    bool ok = !cta_off && l <= 32 && njobs <= 2;
-    for (int j = 0; j < njobs; ++j)
-      ok = ok && jobs[j].w.cta_state && !jobs[j].sharded && !jobs[j].done &&
-           (double)jobs[j].rows * l * 8 <= 6.0 * (1 << 20);
-    if (ok) {
-      sn::CtaJobs cj{};
-      for (int j = 0; j < njobs; ++j) {
-        QrJob& q = jobs[j];
-        cj.j[j] = sn::CtaJob{q.cur, q.nxt, q.rows, ldx, q.w.cta_state,
-                             11.0 * (q.rows_global * l + (double)l * (l + 1)) * kUnit};
-      }
-      sn::cholqr_cta_kernel<<<njobs, sn::THREADS, 0, h->stream>>>(cj, l, kKappaPlain, kMaxQrSteps);
-      CK_LAUNCH();
-      int* outp = reinterpret_cast<int*>(h->pinned + 32);
-      for (int j = 0; j < njobs; ++j) {
-        CK(cudaMemcpyAsync(outp + 4 * j, &jobs[j].w.cta_state->status, sizeof(int), cudaMemcpyDeviceToHost,
-                           h->stream));
-        CK(cudaMemcpyAsync(outp + 4 * j + 1, &jobs[j].w.cta_state->steps, sizeof(int), cudaMemcpyDeviceToHost,
-                           h->stream));
-      }
-      if (extra_flag)
-        CK(cudaMemcpyAsync(h->pinned + 60, extra_flag, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-      sync(h);
-      if (extra_flag && h->pinned[60] != 0.0) fail(h, CORUTV_ERR_NONFINITE, "a contains non-finite entries");
-      for (int j = 0; j < njobs; ++j) {
-        const int status = outp[4 * j];
-        jobs[j].steps = outp[4 * j + 1];
-        if (status == 2) fail(h, CORUTV_ERR_NONFINITE, "sketch contains non-finite entries");
-        if (status == 3) fail(h, CORUTV_ERR_CONVERGENCE, "CholeskyQR did not reach orthogonality");
-        jobs[j].done = true;  // Q in jobs[j].cur
-      }
-      return;
-    }
   }
   // speculative schedule: with the register factor kernel the step rule
   // runs on the device (a finished job's further steps are exact no-ops,
@@ -988,8 +948,17 @@ void qrcp(corutv_handle* h, const double* D, int l, int64_t ldd, double* T, int6
     // 4 threads per column: measured against 1 (64-long dependent DFMA
     // chains, 4x slower) and the smem kernel (C1 l = 15: 25 vs 43 us; C2
     // l = 50: 111 vs 144 us)
-    if (l <= 32) qreg::qrcp_reg_kernel<32, 4><<<1, 128, 0, h->stream>>>(D, l, ldd, T, ldt, qtT, ldq, perm_out, perm32, delta, r_dev);
-    else qreg::qrcp_reg_kernel<64, 4><<<1, 256, 0, h->stream>>>(D, l, ldd, T, ldt, qtT, ldq, perm_out, perm32, delta, r_dev);
+    static const int qg = [] {
+      const char* e = std::getenv("CORUTV_QRCP_REG_G");  // tuning knob: threads per column (2 or 4)
+      return e ? std::atoi(e) : 4;
+    }();
+    if (qg == 2) {
+      if (l <= 32) qreg::qrcp_reg_kernel<32, 2><<<1, 64, 0, h->stream>>>(D, l, ldd, T, ldt, qtT, ldq, perm_out, perm32, delta, r_dev);
+      else qreg::qrcp_reg_kernel<64, 2><<<1, 128, 0, h->stream>>>(D, l, ldd, T, ldt, qtT, ldq, perm_out, perm32, delta, r_dev);
+    } else {
+      if (l <= 32) qreg::qrcp_reg_kernel<32, 4><<<1, 128, 0, h->stream>>>(D, l, ldd, T, ldt, qtT, ldq, perm_out, perm32, delta, r_dev);
+      else qreg::qrcp_reg_kernel<64, 4><<<1, 256, 0, h->stream>>>(D, l, ldd, T, ldt, qtT, ldq, perm_out, perm32, delta, r_dev);
+    }
     CK_LAUNCH();
     return;
   }
@@ -1479,8 +1448,6 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   ar.add(&perm32, (size_t)ldp);
   ar.add(&jstat, 4);
   ar.add(&info, 4);
-  sn::QrState* cta_st;
-  ar.add((char**)&cta_st, 2 * sizeof(sn::QrState));
   ar.commit();
 
   // host input: start the chunked H2D copy before anything else
@@ -1567,7 +1534,6 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   jobs[0].sharded = sharded;
   jobs[0].w = QrWork{G, rinvT, gwork, ws, info};
   jobs[0].w.qd = reinterpret_cast<int*>(info + 1);
-  jobs[0].w.cta_state = cta_st;
   jobs[1].cur = c2;
   jobs[1].nxt = C2a;
   jobs[1].rows = n;
@@ -1575,7 +1541,6 @@ void decompose(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t 
   jobs[1].sharded = false;
   jobs[1].w = QrWork{G2, rinvT2, gwork2, ws_qr2 ? ws_qr2 : ws, info + 2};
   jobs[1].w.qd = reinterpret_cast<int*>(info + 3);
-  jobs[1].w.cta_state = cta_st + 1;
   cholqr_multi(h, jobs, 2, l, ldp, flagd);
   double* Q1 = jobs[0].cur;
   double* Q2 = jobs[1].cur;
@@ -1678,8 +1643,6 @@ void tsr(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, i
   ar.add(&flag, 4);
   ar.add(&jstat, 4);
   ar.add(&info, 4);
-  sn::QrState* cta_st;
-  ar.add((char**)&cta_st, 2 * sizeof(sn::QrState));
   // host input: z = A' phi split-K slices as the row chunks land
   const GemmPlan zplan = plan_gemm(h, n, l, m, true);
   double* ws2 = nullptr;
@@ -1740,7 +1703,6 @@ void tsr(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, i
   jobs[0].sharded = false;
   jobs[0].w = QrWork{G, rinvT, gwork, ws, info};
   jobs[0].w.qd = reinterpret_cast<int*>(info + 1);
-  jobs[0].w.cta_state = cta_st;
   jobs[1].cur = Z;
   jobs[1].nxt = Zb;
   jobs[1].rows = n;
@@ -1748,7 +1710,6 @@ void tsr(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, i
   jobs[1].sharded = false;
   jobs[1].w = QrWork{G2, rinvT2, gwork2, ws, info + 2};
   jobs[1].w.qd = reinterpret_cast<int*>(info + 3);
-  jobs[1].w.cta_state = cta_st + 1;
   cholqr_multi(h, jobs, 2, l, ldp, flagd);
   const double* Q1 = jobs[0].cur;
   const double* Q2 = jobs[1].cur;
@@ -1800,14 +1761,16 @@ void lowrank_op(corutv_handle* h, int mode, const double* u, const double* t, co
   // SM, so one CTA's TMA mainloop overlaps another's memory-bound epilogue
   int n_tiles = (int)((cols + 63) / 64);
   int J = (int)std::min<int64_t>(4, std::max<int64_t>(1, (cols + 16 * n_tiles - 1) / (16 * n_tiles)));
-  // ALM update: 128 x 32 tiles at three CTAs per SM (A/B knob CORUTV_ALM_J=4
-  // restores round 1's 128 x 64 tiles at two)
+  // ALM update with r > 0: 128 x 32 tiles at three CTAs per SM, so the
+  // rank-r products and streaming epilogues of co-resident CTAs interleave
+  // (r = 50: 0.95 vs 1.01 ms; r = 20: 0.77 vs 0.83 ms); r = 0 keeps round
+  // 1's 128 x 64 tiles at two (0.66 ms).  A/B knob: CORUTV_ALM_J=4.
   static const int alm_j = [] {
     const char* e = std::getenv("CORUTV_ALM_J");
     return e ? std::atoi(e) : 2;
   }();
   int minb = 2;
-  if (mode == gemm::LR_ALM && alm_j == 2 && cols >= 32) {
+  if (mode == gemm::LR_ALM && alm_j == 2 && cols >= 32 && r > 0) {
     n_tiles = (int)((cols + 31) / 32);
     J = 2;
     minb = 3;

@@ -648,104 +648,4 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (threadIdx.x == 0 && last_launch && !__ldcg(&st->finish) && __ldcg(&st->status) == 0) st->status = 3;
 }
 
-// ----------------------------------------------------------------------
-// The whole adaptive CholeskyQR of a SMALL sketch (b <= 32 columns, rows
-// resident in L2) in one CTA per matrix, every step in one launch:
-// householder_qr(C).q of sketch.py:198-199 for the narrow cores (C1:
-// 1000 x 15, the ALM iterations' l <= 32 sketches).  Per step one pass over
-// the rows in RCH-row chunks: x <- x R^-1 (the pending factor) into the
-// other buffer and the Gram of the new rows on the tensor pipe; then the
-// CTA factors that Gram (factor_step: plain while kappa_F <= 1e6, else the
-// Fukaya shift; two consecutive plain steps finish).  The first pass only
-// takes the Gram.  Replaces per step a split-K Gram GEMM, its finalize, the
-// factor launch and the X R^-1 GEMM, and the host round trips between steps.
-// The result always ends in x (copied back from xn after an odd number of
-// applies); st->steps / status as cholqr_multi's (3: not converged).
-struct CtaJob {
-  double* x;
-  double* xn;
-  int64_t rows;
-  int64_t ldx;
-  QrState* st;
-  double shift_coeff;
-};
-
-struct CtaJobs {
-  CtaJob j[2];
-};
-
-__global__ void __launch_bounds__(THREADS, 1)
-    cholqr_cta_kernel(CtaJobs jobs, int b, double kappa_max, int max_steps) {
-  __shared__ RowSmem sm;
-  const CtaJob jb = jobs.j[blockIdx.x];
-  QrState* st = jb.st;
-  if (threadIdx.x == 0) reset_qr_state(st);
-  auto load_chunk = [&](const double* src, int64_t c0, int nr, int nr4) {
-    for (int e = threadIdx.x; e < nr4 * B; e += THREADS) {
-      const int r = e / B, c = e % B;
-      sm.u.x[r * LDX + c] = (r < nr && c < b) ? src[(c0 + r) * jb.ldx + c] : 0.0;
-    }
-  };
-  auto gram_to_smem = [&](const double (&acc)[2][2]) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int r8 = lane >> 2, c4 = lane & 3;
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const int q = 2 * warp + t, bi = q >> 2, bj = q & 3;
-#pragma unroll
-      for (int e = 0; e < 2; ++e) sm.u.f.G[(bi * 8 + r8) * B + bj * 8 + 2 * c4 + e] = acc[t][e];
-    }
-  };
-  // step 0: Gram of x
-  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-  for (int64_t c0 = 0; c0 < jb.rows; c0 += RCH) {
-    const int nr = (int)min((int64_t)RCH, jb.rows - c0), nr4 = (nr + 3) & ~3;
-    __syncthreads();
-    load_chunk(jb.x, c0, nr, nr4);
-    __syncthreads();
-    gram_chunk(sm.u.x, nr4, acc);
-  }
-  __syncthreads();
-  gram_to_smem(acc);
-  __syncthreads();
-  factor_step(sm.u.f.G, B, b, jb.shift_coeff, kappa_max, st, sm.u.f.W, sm.red, sm.rowj, sm.piv);
-  __syncthreads();
-  double* cur = jb.x;
-  double* nxt = jb.xn;
-  int applied = 0;
-  for (int step = 0; step < max_steps; ++step) {
-    if (__ldcg(&st->status) == 2) break;  // non-finite (uniform: read after a barrier)
-    for (int e = threadIdx.x; e < B * B; e += THREADS) sm.Ri[(e / B) * (B + 1) + e % B] = __ldcg(st->rinv + e);
-    double g[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-    for (int64_t c0 = 0; c0 < jb.rows; c0 += RCH) {
-      const int nr = (int)min((int64_t)RCH, jb.rows - c0), nr4 = (nr + 3) & ~3;
-      __syncthreads();
-      load_chunk(cur, c0, nr, nr4);
-      __syncthreads();
-      apply_rinv_chunk(sm.u.x, sm.Ri, nr4);
-      store_chunk(sm.u.x, nr, b, c0, nxt, jb.ldx, nullptr, 0);
-      gram_chunk(sm.u.x, nr4, g);
-    }
-    double* tsw = cur;
-    cur = nxt;
-    nxt = tsw;
-    ++applied;
-    __syncthreads();
-    if (__ldcg(&st->finish)) break;
-    gram_to_smem(g);
-    __syncthreads();
-    factor_step(sm.u.f.G, B, b, jb.shift_coeff, kappa_max, st, sm.u.f.W, sm.red, sm.rowj, sm.piv);
-    __syncthreads();
-    if (step + 1 == max_steps && threadIdx.x == 0 && !__ldcg(&st->finish) && st->status == 0) st->status = 3;
-  }
-  __syncthreads();
-  if (applied & 1) {  // the result is in xn: copy it back into x
-    __threadfence_block();
-    for (int64_t e = threadIdx.x; e < jb.rows * b; e += THREADS) {
-      const int64_t r = e / b, c = e % b;
-      jb.x[r * jb.ldx + c] = __ldcg(jb.xn + r * jb.ldx + c);
-    }
-  }
-}
-
 }  // namespace sn
