@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(LM * G, 1)
                     double* __restrict__ qtT, int64_t ldq, long long* perm_out, int* perm32, double delta,
                     int* r_out) {
   constexpr int NT = LM * G, RPT = LM / G, NWP = NT / 32;
-  static_assert(LM % 32 == 0 && 32 % G == 0 && LM % G == 0, "shape");
+  static_assert(LM % 32 == 0 && 32 % G == 0 && LM % G == 0 && G > 1, "shape");
   __shared__ Shared<LM> sm;
   const int tid = threadIdx.x, lane = tid & 31;
   const int c = tid / G, g = tid % G;
@@ -109,22 +109,14 @@ __global__ void __launch_bounds__(LM * G, 1)
     }
     const int p = bq < l ? bq : j, pc = bq < l ? bc : sm.at[cb][j];
     const int cj = sm.at[cb][j];
-    // reflector of x = R[j:, pc] (every thread, from the published tail;
-    // G == 1 re-reads it from shared memory instead of holding a copy)
-    constexpr int XR = G > 1 ? RPT : 1;
-    double xr[XR];
-    auto xval = [&](int k) -> double {
-      const int i = g + G * k;
-      if constexpr (G > 1) return xr[k];
-      return (i > j && i < l) ? sm.rs[i][pc] : 0.0;
-    };
+    // reflector of x = R[j:, pc] (every thread, from the published tail)
+    double xr[RPT];
     double t2p = 0.0;
 #pragma unroll
     for (int k = 0; k < RPT; ++k) {
       const int i = g + G * k;
-      const double x = (i > j && i < l) ? sm.rs[i][pc] : 0.0;
-      if constexpr (G > 1) xr[k] = x;
-      t2p = fma(x, x, t2p);
+      xr[k] = (i > j && i < l) ? sm.rs[i][pc] : 0.0;
+      t2p = fma(xr[k], xr[k], t2p);
     }
     const double t2 = gsum<G>(t2p);
     const double x0 = sm.rs[j][pc];
@@ -151,7 +143,7 @@ __global__ void __launch_bounds__(LM * G, 1)
     if (refl) {  // uniform; the group sums run in every lane (shuffles)
       double s = 0.0;
 #pragma unroll
-      for (int k = 0; k < RPT; ++k) s = fma(xval(k), r[k], s);
+      for (int k = 0; k < RPT; ++k) s = fma(xr[k], r[k], s);
       if (g == jo) {
 #pragma unroll
         for (int k = 0; k < RPT; ++k)
@@ -162,7 +154,7 @@ __global__ void __launch_bounds__(LM * G, 1)
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
           const int i = g + G * k;
-          if (i > j) r[k] = fma(-xval(k), w, r[k]);
+          if (i > j) r[k] = fma(-xr[k], w, r[k]);
           else if (i == j) r[k] = fma(-v0, w, r[k]);
         }
       }
@@ -230,19 +222,12 @@ __global__ void __launch_bounds__(LM * G, 1)
     const double v0 = sm.vhead[j], tj = sm.tau[j];
     const int jo = j % G, jk = j / G;
     double s = 0.0;
-    constexpr int XQ = G > 1 ? RPT : 1;
-    double xr[XQ];
-    auto xq = [&](int k) -> double {
-      const int i = g + G * k;
-      if constexpr (G > 1) return xr[k];
-      return (i > j && i < l) ? sm.rs[i][pc] : 0.0;
-    };
+    double xr[RPT];
 #pragma unroll
     for (int k = 0; k < RPT; ++k) {
       const int i = g + G * k;
-      const double x = (i > j && i < l) ? sm.rs[i][pc] : 0.0;
-      if constexpr (G > 1) xr[k] = x;
-      s = fma(x, r[k], s);
+      xr[k] = (i > j && i < l) ? sm.rs[i][pc] : 0.0;
+      s = fma(xr[k], r[k], s);
     }
     if (g == jo) {
 #pragma unroll
@@ -254,7 +239,7 @@ __global__ void __launch_bounds__(LM * G, 1)
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
         const int i = g + G * k;
-        if (i > j) r[k] = fma(-xq(k), w, r[k]);
+        if (i > j) r[k] = fma(-xr[k], w, r[k]);
         else if (i == j) r[k] = fma(-v0, w, r[k]);
       }
     }
