@@ -26,7 +26,6 @@
 #include "common.cuh"
 #include "gemm.cuh"
 #include "qrcp_reg.cuh"
-#include "dual_sketch.cuh"
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
@@ -1648,14 +1647,6 @@ void tsr(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, i
   const GemmPlan zplan = plan_gemm(h, n, l, m, true);
   double* ws2 = nullptr;
   if (feed && zplan.splits > 1) ar.add(&ws2, (size_t)zplan.splits * n * round_up(l, 2) + 16);
-  // resident A and l <= 16: both sketches from one pass over A
-  // (dual_sketch.cuh); z partials per CTA, at most ~4 % of A's bytes
-  static const bool dual_off = std::getenv("CORUTV_DUAL_OFF") != nullptr;  // A/B knob
-  const int msubs = (int)((m + dual::BM - 1) / dual::BM);
-  const int dual_grid = std::min<int>(msubs, std::max<int>(h->num_sms, (msubs + dual::YMAX - 1) / dual::YMAX));
-  const bool use_dual = !feed && !dual_off && l <= 16 && (double)dual_grid * n * 16 <= 0.04 * (double)m * n + 4e6;
-  double* zpart = nullptr;
-  if (use_dual) ar.add(&zpart, (size_t)dual_grid * n * 16);
   ar.commit();
   Feeder fd{h, feed, m, n, lda};
   if (feed) {
@@ -1696,22 +1687,6 @@ void tsr(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, i
     }
     if (ws2) finalize_splits(h, zplan, n, l, ws2, Z, ldp, nullptr, 0);
     else run_gemm(h, true, n, l, m, A, ldA, Phi, ldp, Z, ldp, nullptr, 0, ws);
-  } else if (use_dual) {
-    TagScope ts(h, 1);
-    const CUtensorMap ma = make_map(h, A, n, m, ldA, dual::BM);
-    const CUtensorMap mp = make_map(h, PsiT, n, l, ldn, 16);
-    const CUtensorMap mf = make_map(h, Phi, l, m, ldp, dual::BM);
-    set_smem(h, dual::dual_sketch_kernel, dual::SMEM);
-    {
-      ProfScope ps(h, h->tag, 4.0 * m * n * (double)l);
-      dual::dual_sketch_kernel<<<dual_grid, dual::THREADS, dual::SMEM, h->stream>>>(ma, mp, mf, m, n, msubs, Y, ldp,
-                                                                                  zpart, flag);
-      CK_LAUNCH();
-    }
-    int nb, tb;
-    launch_grid_1d(n * l, &nb, &tb);
-    aux::splitk_finalize_kernel<<<nb, tb, 0, h->stream>>>(zpart, dual_grid, n * 16, n, l, 16, Z, ldp, nullptr, 0);
-    CK_LAUNCH();
   } else {
     TagScope ts(h, 1);
     run_gemm(h, false, m, l, n, A, ldA, PsiT, ldn, Y, ldp, nullptr, 0, ws, flag);  // y = A psi
