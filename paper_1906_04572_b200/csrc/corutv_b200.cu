@@ -1989,8 +1989,20 @@ void spectral_norm_fused(corutv_handle* h, const double* A, int64_t ldA, int64_t
     if (dbg) std::fprintf(stderr, "[snorm fused] it %d est %.17g lam %.17g rel %.3e\n", it, est, h->pinned[8],
                           prev > 0 ? std::fabs(est - prev) / est : 0.0);
     if (iters) *iters = it + 1;
+    const bool stop = est == 0.0 || std::fabs(est - prev) <= 0.02 * tol * est;
+    if (stop && dbg) {
+      // the last iteration's latency-kernel anatomy (snorm.cuh QrState::prof)
+      unsigned long long pf[8];
+      sync(h);
+      CK(cudaMemcpy(pf, qst->prof, sizeof(pf), cudaMemcpyDeviceToHost));
+      std::fprintf(stderr,
+                   "[snorm prof] finalize<1>: rows %.1f us, reduce %.1f us, factor %.1f us | apply: rows %.1f us, "
+                   "reduce %.1f us, factor %.1f us | fin1 start -> apply start %.1f us\n",
+                   (pf[5] - pf[4]) * 1e-3, (pf[6] - pf[5]) * 1e-3, (pf[7] - pf[6]) * 1e-3, (pf[1] - pf[0]) * 1e-3,
+                   (pf[2] - pf[1]) * 1e-3, (pf[3] - pf[2]) * 1e-3, (pf[0] - pf[4]) * 1e-3);
+    }
     if (est == 0.0) { *out = 0.0; return; }
-    if (std::fabs(est - prev) <= 0.02 * tol * est) { *out = est; return; }
+    if (stop) { *out = est; return; }
     prev = est;
   }
   *out = prev;

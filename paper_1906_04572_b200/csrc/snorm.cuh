@@ -37,7 +37,16 @@ struct QrState {
   int steps;
   unsigned ticket;        // last-CTA election of a finishing apply (reset by it)
   unsigned tickets[16];   // two-level Gram reduction: [0] final, [1 + g] group g
+  // %globaltimer stamps of the last launch (apply [0..3], finalize<1>
+  // [4..7]): start, slowest CTA's rows done, reduction done, factor done
+  unsigned long long prof[8];
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 struct WState {
   unsigned tickets[16];
@@ -572,18 +581,26 @@ __global__ void __launch_bounds__(THREADS, 1)
                     QrState* st, double shift_coeff, double kappa_max, int use_pending) {
   __shared__ RowSmem sm;
   if (MODE == 0) load_pending_rinv(sm, st, use_pending);
-  if (MODE == 1 && blockIdx.x == 0 && threadIdx.x == 0) reset_qr_state(st);  // visible to the later applies
+  if (MODE == 1 && blockIdx.x == 0 && threadIdx.x == 0) {
+    reset_qr_state(st);  // visible to the later applies
+    st->prof[4] = gtimer();
+    st->prof[1] = 0;
+  }
   int64_t r0, r1;
   cta_rows(rows, &r0, &r1);
   double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
   __syncthreads();
   finalize_rows<MODE>(sm, ws, splits, sstride, ldw, r0, r1, b, out, ldo, outT, ldoT, acc);
   gram_store(acc, part, blockIdx.x);
+  if (MODE == 1 && threadIdx.x == 0) atomicMax(&st->prof[5], gtimer());
   if (!last_cta_reduce(part, part2, b, tickets, sm.u.f.G, blockIdx.x, gridDim.x)) return;
   if (MODE == 0) {
     for (int e = threadIdx.x; e < B * B; e += THREADS) lam[e] = sm.u.f.G[e];
   } else {
+    if (threadIdx.x == 0) st->prof[6] = gtimer();
     factor_step(sm.u.f.G, B, b, shift_coeff, kappa_max, st, sm.u.f.W, sm.red, sm.rowj, sm.piv);
+    __syncthreads();
+    if (threadIdx.x == 0) st->prof[7] = gtimer();
   }
 }
 
@@ -616,6 +633,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                  double kappa_max, int last_launch) {
   __shared__ RowSmem sm;
   if (*((volatile int*)&st->finish) || *((volatile int*)&st->status)) return;  // uniform: earlier launches
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->prof[0] = gtimer();
   for (int e = threadIdx.x; e < B * B; e += THREADS) sm.Ri[(e / B) * (B + 1) + e % B] = __ldcg(st->rinv + e);
   int64_t r0, r1;
   cta_rows(rows, &r0, &r1);
@@ -641,9 +659,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
   }
   gram_store(acc, part, blockIdx.x);
+  if (threadIdx.x == 0) atomicMax(&st->prof[1], gtimer());
   if (!last_cta_reduce(part, part2, b, st->tickets, sm.u.f.G, blockIdx.x, gridDim.x)) return;
+  if (threadIdx.x == 0) st->prof[2] = gtimer();
   factor_step(sm.u.f.G, B, b, shift_coeff, kappa_max, st, sm.u.f.W, sm.red, sm.rowj, sm.piv);
   __syncthreads();
+  if (threadIdx.x == 0) {
+    st->prof[3] = gtimer();
+    st->prof[5] = 0;  // the next finalize<1>'s max-stamp starts over
+  }
   // the launch budget is spent and another step would be needed
   if (threadIdx.x == 0 && last_launch && !__ldcg(&st->finish) && __ldcg(&st->status) == 0) st->status = 3;
 }
