@@ -163,7 +163,7 @@ __device__ void chol_factor_block(const double* G, int l, int64_t ldg, double sh
 __global__ void __launch_bounds__(512, 1)
     chol_factor_kernel(const double* __restrict__ G, int l, int64_t ldg, double shift_coeff,
                        int allow_plain, double kappa_max, double* __restrict__ rinvT,
-                       int64_t ldr, double* gwork, int use_smem, CholInfo* info) {
+                       int64_t ldr, double* gwork, int use_smem, CholInfo* info, int* qd) {
   extern __shared__ double dsm[];
   __shared__ double red[NWARPS];
   // [G | I] always in shared memory here (the host launches this kernel only
@@ -171,7 +171,24 @@ __global__ void __launch_bounds__(512, 1)
   // an LDS/STS rather than a generic LD/ST
   (void)use_smem;
   (void)gwork;
+  // qd (optional, speculative schedule): {plain, done, status, steps} of
+  // cholqr_multi's rule on the device (as creg::chol_reg_kernel); once done
+  // the step is an exact no-op, R^-1 = I
+  if (qd && *((volatile int*)&qd[1])) {
+    for (int e = threadIdx.x; e < l * l; e += blockDim.x) {
+      const int i = e / l, k = e % l;
+      rinvT[(int64_t)i * ldr + k] = (i == k) ? 1.0 : 0.0;
+    }
+    return;
+  }
   chol_factor_block(G, l, ldg, shift_coeff, allow_plain, kappa_max, rinvT, ldr, info, dsm, red);
+  if (qd && threadIdx.x == 0) {
+    const int plain = info->shifted ? 0 : qd[0] + 1;
+    qd[0] = plain;
+    qd[3] += 1;
+    if (info->status == 2) qd[2] = 2;
+    if (info->status != 0 || plain == 2) qd[1] = 1;
+  }
 }
 
 // ------------------------------------------------------------------- QRCP
