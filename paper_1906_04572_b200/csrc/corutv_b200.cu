@@ -2048,9 +2048,14 @@ void spectral_norm_fused(corutv_handle* h, const double* A, int64_t ldA, int64_t
     const bool stop = est == 0.0 || std::fabs(est - prev) <= 0.02 * tol * est;
     if (stop && dbg) {
       // the last iteration's latency-kernel anatomy (snorm.cuh QrState::prof)
-      unsigned long long pf[8];
+      unsigned long long pf[8], ff[8];
       sync(h);
       CK(cudaMemcpy(pf, qst->prof, sizeof(pf), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(ff, qst->fprof, sizeof(ff), cudaMemcpyDeviceToHost));
+      std::fprintf(stderr, "[snorm prof] last factor step: trace %.2f us, attempt 1 %.2f us, attempt 2 %.2f us, "
+                           "R^-1 store %.2f us, shifted %llu\n",
+                   (ff[1] - ff[0]) * 1e-3, (ff[2] - ff[1]) * 1e-3, (ff[3] - ff[2]) * 1e-3, (ff[4] - ff[3]) * 1e-3,
+                   ff[6]);
       std::fprintf(stderr,
                    "[snorm prof] finalize<1>: rows %.1f us, reduce %.1f us, factor %.1f us | apply: rows %.1f us, "
                    "reduce %.1f us, factor %.1f us | fin1 start -> apply start %.1f us\n",

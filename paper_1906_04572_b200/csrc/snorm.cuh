@@ -40,6 +40,7 @@ struct QrState {
   // %globaltimer stamps of the last launch (apply [0..3], finalize<1>
   // [4..7]): start, slowest CTA's rows done, reduction done, factor done
   unsigned long long prof[8];
+  unsigned long long fprof[8];  // factor_step: entry, trace, attempt 1, attempt 2, R^-1 stored, end; shifted
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -156,8 +157,10 @@ __device__ bool cta_chol_aug(const double* Gs, int ldg, int b, double shift, dou
 __device__ void factor_step(const double* Gs, int ldg, int b, double shift_coeff, double kappa_max,
                             QrState* st, double* W, double* red, double* rowj, double* piv) {
   const int tid = threadIdx.x;
+  unsigned long long f0 = tid == 0 ? gtimer() : 0, f1 = 0, f2 = 0, f3 = 0;
   double tr = 0.0;
   for (int i = 0; i < b; ++i) tr += Gs[i * ldg + i];  // same order in every thread
+  if (tid == 0) f1 = gtimer();
   int shifted = 0, status = 0;
   double kappa = 1.0;
   bool ident = false;
@@ -169,12 +172,14 @@ __device__ void factor_step(const double* Gs, int ldg, int b, double shift_coeff
     double nr2, ni2;
     bool ok = cta_chol_aug(Gs, ldg, b, 0.0, W, red, rowj, piv, nr2, ni2);
     kappa = sqrt(nr2) * sqrt(ni2);
+    if (tid == 0) f2 = gtimer();
     if (!ok || !(kappa <= kappa_max)) {
       shifted = 1;
       ok = cta_chol_aug(Gs, ldg, b, shift_coeff * tr, W, red, rowj, piv, nr2, ni2);
       kappa = sqrt(nr2) * sqrt(ni2);
       if (!ok) status = 2;
     }
+    if (tid == 0) f3 = gtimer();
   }
   // R^-1[k][c] = (R^-T)[c][k]
   for (int e = tid; e < B * B; e += THREADS) {
@@ -182,6 +187,13 @@ __device__ void factor_step(const double* Gs, int ldg, int b, double shift_coeff
     st->rinv[e] = ident ? (k == c ? 1.0 : 0.0) : ((k <= c) ? W[c * LDA + B + k] : 0.0);
   }
   if (tid == 0) {
+    const unsigned long long f4 = gtimer();
+    st->fprof[0] = f0;
+    st->fprof[1] = f1;
+    st->fprof[2] = f2;
+    st->fprof[3] = f3;
+    st->fprof[4] = f4;
+    st->fprof[6] = shifted;
     st->kappa = kappa;
     st->steps = __ldcg(&st->steps) + 1;
     if (status == 2) {
