@@ -1867,6 +1867,10 @@ void lowrank_op(corutv_handle* h, int mode, const double* u, const double* t, co
   CUtensorMap mw = make_map(h, Wt, std::max(r, 1), cols, ldr, 16 * J);
   p.part_sum = part;
   p.part_cnt = cnt;
+  // r mod 16 in 1..8: the last k tile's second 8-value group is all TMA
+  // zero fill, the mainloop skips it (r = 50: 7 DMMA groups instead of 8)
+  static const bool full_k = std::getenv("CORUTV_LR_FULLK") != nullptr;  // A/B knob
+  p.np_last = (!full_k && r % 16 >= 1 && r % 16 <= 8) ? 1 : 2;
   // double2 epilogue accesses need an even ld and 16-byte aligned bases (a
   // caller's view such as X[:, 1:] is only 8-byte aligned)
   {
@@ -2968,6 +2972,15 @@ int corutv_alm_update(corutv_handle* hh, const double* m_mat, double* s, double*
   p.mu = mu;
   p.lam_over_mu = lam_over_mu;
   p.mu_next = mu_next;
+  // y / mu and y' / mu_next by gemm::div_const (bitwise the IEEE quotient);
+  // A/B knob: CORUTV_ALM_PLAIN_DIV=1 keeps the division instruction sequence
+  static const bool plain_div = std::getenv("CORUTV_ALM_PLAIN_DIV") != nullptr;
+  auto recip = [](double b) {
+    const double ab = std::fabs(b);
+    return (!plain_div && ab >= 0x1p-200 && ab <= 0x1p200) ? 1.0 / b : 0.0;
+  };
+  p.inv_mu = recip(mu);
+  p.inv_mu_next = recip(mu_next);
   double o[2] = {0, 0};
   lowrank_op(h, gemm::LR_ALM, u, t, v, rows, cols, ell, r, p, o);
   if (zeta2_host) *zeta2_host = o[0];

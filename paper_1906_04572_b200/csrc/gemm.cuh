@@ -174,9 +174,11 @@ template <int J, bool MM, bool CHECK, int S = num_stages(J), int WN = 2>
 __device__ __forceinline__ void mainloop(const Smem& sm, const CUtensorMap* mapA,
                                          const CUtensorMap* mapB, int m0, int n0, int kt0,
                                          int kt1, Acc<J>& acc, int wm, int wn, int lane, int nvf,
-                                         int mvf, bool& bad, int mm3d = 0, int i0 = 0) {
+                                         int mvf, bool& bad, int mm3d = 0, int i0 = 0, int np_last = 2) {
   // i0: ring iterations already run by this CTA (stream-K: a second
   // segment continues the ring where the first left it)
+  // np_last (KK only): 8-value k groups of the LAST k tile that hold any
+  // k < K; 1 skips the group TMA zero-filled (K mod 16 in 1..8)
   (void)nvf;
   (void)mvf;
   const int nkt = kt1 - kt0;
@@ -222,8 +224,10 @@ __device__ __forceinline__ void mainloop(const Smem& sm, const CUtensorMap* mapA
     const double* sa = sm.a + st * (bm_of(WN) * BK);
     const double* sb = sm.b + st * (nb16_of(J, WN) * 16 * BK);
     if (!MM) {
+      const int np = (i == nkt - 1) ? np_last : 2;
 #pragma unroll
       for (int p = 0; p < 2; ++p) {
+        if (p >= np) break;
         double2 a2[4], b2[J];
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) {
@@ -422,6 +426,27 @@ __global__ void __launch_bounds__(THREADS, MINB)
 // each 128 x 16J tile in registers.
 enum LrMode { LR_STORE = 0, LR_ALM = 1, LR_RESID = 2 };
 
+// a / b, correctly rounded (bitwise the IEEE quotient), for a divisor that is
+// the same for every element: rb = RN(1 / b) comes from the host.  q0 = a rb
+// is within 1.5 ulp; one residual correction makes it faithful, and by
+// Markstein's theorem (rb the correctly rounded reciprocal, q faithful, the
+// residual a - b q exact in an FMA) the second correction rounds to RN(a / b).
+// 5 FP64 operations instead of the ~14-instruction division sequence.  Outside
+// the exponent range where the residuals are exact (|a| in [2^-800, 2^800];
+// includes a = 0, whose sign the corrections would lose) or when the host
+// passes rb = 0 (b outside [2^-200, 2^200]) the plain division runs.
+CU_DEV double div_const(double a, double b, double rb) {
+  const uint32_t e = (static_cast<uint32_t>(__double2hiint(a)) >> 20) & 0x7ffu;
+  if (rb != 0.0 && e - 223u <= 1600u) {
+    const double q0 = a * rb;
+    const double r0 = fma(-b, q0, a);
+    const double q1 = fma(r0, rb, q0);
+    const double r1 = fma(-b, q1, a);
+    return fma(r1, rb, q1);
+  }
+  return a / b;
+}
+
 struct LrParams {
   int64_t ld;            // leading dimension of all n x n operands
   const double* m_mat;   // ALM: M ; RESID: A
@@ -429,6 +454,8 @@ struct LrParams {
   double* y;             // ALM: Y in/out
   double* g_next;        // ALM: next G out ; STORE: L out
   double mu, lam_over_mu, mu_next;
+  double inv_mu, inv_mu_next;  // RN(1 / mu), RN(1 / mu_next) for div_const; 0: use the plain division
+  int np_last;           // mainloop: k groups of the last k tile (1 when r mod 16 is in 1..8)
   double* part_sum;      // per-CTA partial sum of squares
   long long* part_cnt;   // per-CTA partial nnz
   int vec;               // 16-byte (double2) accesses allowed: ld even and every
@@ -472,7 +499,8 @@ __global__ void __launch_bounds__(THREADS, MINB)
   Acc<J> acc;
   acc.zero();
   bool bad = false;
-  mainloop<J, false, false, LR_STAGES>(sm, &mapU, &mapW, m0, n0, 0, t.k_tiles, acc, wm, wn, lane, nvf, mvf, bad);
+  mainloop<J, false, false, LR_STAGES>(sm, &mapU, &mapW, m0, n0, 0, t.k_tiles, acc, wm, wn, lane, nvf, mvf, bad, 0, 0,
+                                       p.np_last);
 
   // Stage the 128 x 16J tile of L in shared memory (the pipeline buffers are
   // free now), then stream it row by row: each warp owns rows, lanes cover
@@ -554,13 +582,13 @@ __global__ void __launch_bounds__(THREADS, MINB)
         } else if (MODE == LR_ALM) {
           // rpca.py:211-214, operation order mirrored from the numpy source
           const double mm = mvv[e], yy = yvv[e];
-          const double g = (mm - l) + yy / p.mu;
+          const double g = (mm - l) + div_const(yy, p.mu, p.inv_mu);
           const double ag = fabs(g) - p.lam_over_mu;
           const double sg = (g > 0.0) ? 1.0 : ((g < 0.0) ? -1.0 : g);
           sv[e] = sg * fmax(ag, 0.0);
           const double z = (mm - l) - sv[e];
           yn[e] = yy + p.mu * z;
-          gv[e] = (mm - sv[e]) + yn[e] / p.mu_next;
+          gv[e] = (mm - sv[e]) + div_const(yn[e], p.mu_next, p.inv_mu_next);
           ssum = fma(z, z, ssum);
           cnt += (fabs(sv[e]) > 1e-12) ? 1 : 0;
         }

@@ -537,6 +537,55 @@ def test_alm_update_matches_torch_formula():
     assert nnz.value == int((s_ref.abs() > 1e-12).sum())
 
 
+@pytest.mark.parametrize("mu,mu_next", [(0.7, 1.05), (3.0, 4.5), (1.2345678901234567e-3, 1.8518518351851852e-3),
+                                         (1.9999999999999998, 2.9999999999999996), (1e7, 1.5e7),
+                                         (1e-250, 1e250)])
+def test_alm_update_division_is_ieee_bitwise(mu, mu_next):
+    """The fused update divides Y by the per-call constants mu and mu_next
+    (rpca.py:211, 216) with gemm::div_const (reciprocal + two FMA residual
+    corrections).  At r = 0 (L = 0 exactly) S = shrink(M + Y / mu) and
+    G = (M - S) + Y' / mu_next contain no contractible product, so they must
+    equal torch's IEEE results bit for bit -- including zeros, denormals,
+    huge entries and divisors outside the fast range (the last case)."""
+    rows, cols, ell = 2048, 1536, 4
+    g = torch.Generator(device="cuda")
+    g.manual_seed(77)
+    M = torch.randn((rows, cols), generator=g, dtype=torch.float64, device="cuda")
+    Y = torch.randn((rows, cols), generator=g, dtype=torch.float64, device="cuda")
+    # spread the dividends over many binades, plant special values
+    Y *= torch.exp2(torch.randint(-60, 60, (rows, cols), generator=g, device="cuda").double())
+    Y[0, :8] = torch.tensor([0.0, -0.0, 5e-324, -2.5e-310, 1e-300, 1.7e308, -1.2e305, 1.0], dtype=torch.float64)
+    # mantissas next to 1 and 2 (the hard cases for a reciprocal product)
+    Y[1, :4] = torch.tensor([1.0000000000000002, 1.9999999999999998, 0.9999999999999999, 3.0000000000000004],
+                            dtype=torch.float64)
+    M[0, :8] = 0.0
+    u = torch.zeros((rows, ell), dtype=torch.float64, device="cuda")
+    t = torch.zeros((ell, ell), dtype=torch.float64, device="cuda")
+    v = torch.zeros((cols, ell), dtype=torch.float64, device="cuda")
+    lam_over_mu = 0.05 / mu if 1e-200 < mu < 1e200 else 0.0
+    S = torch.empty_like(M); G = torch.empty_like(M); Y2 = Y.clone()
+    import ctypes
+    z2, nnz = ctypes.c_double(0), ctypes.c_int64(0)
+    h = _lib.handle(0)
+    h.call("corutv_alm_update", M.data_ptr(), S.data_ptr(), Y2.data_ptr(), G.data_ptr(), rows, cols,
+           u.data_ptr(), t.data_ptr(), v.data_ptr(), ell, 0, mu, lam_over_mu, mu_next,
+           ctypes.byref(z2), ctypes.byref(nnz))
+    # a DEVICE tensor divisor: torch turns division by a Python / CPU scalar
+    # into a multiplication by its reciprocal, which is not the IEEE quotient
+    mu_t = torch.tensor(mu, dtype=torch.float64, device="cuda")
+    mun_t = torch.tensor(mu_next, dtype=torch.float64, device="cuda")
+    q_np = Y[:64].cpu().numpy() / mu          # numpy: the IEEE quotient
+    assert np.array_equal((Y[:64] / mu_t).cpu().numpy().view(np.int64), q_np.view(np.int64))
+    g2 = M + Y / mu_t
+    s_ref = torch.sign(g2) * torch.clamp_min(g2.abs() - lam_over_mu, 0.0)
+    # (a zero's sign is sign(g)'s in the kernel, + in torch.sign: equal as values)
+    same = (S.view(torch.int64) == s_ref.view(torch.int64)) | ((S == 0) & (s_ref == 0)) | ~torch.isfinite(s_ref)
+    assert bool(same.all()), int((~same).sum())
+    g_ref = (M - S) + Y2 / mun_t
+    same = (G.view(torch.int64) == g_ref.view(torch.int64)) | ~torch.isfinite(g_ref)
+    assert bool(same.all()), int((~same).sum())
+
+
 @pytest.mark.parametrize("chunk_bytes", [None, 1 << 20])
 def test_corutv_file_streams_bitwise(tmp_path, monkeypatch, chunk_bytes):
     """corutv of a CRUTVMAT file streamed disk -> pinned staging
