@@ -16,7 +16,9 @@ from pathlib import Path
 from .errors import ConvergenceError, CorutvError
 
 LIB_NAME = "libcorutv_b200.so"
-LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
+# CORUTV_LIB: an alternative build of the same library (A/B measurements)
+LIB_PATH = Path(os.environ["CORUTV_LIB"]).resolve() if os.environ.get("CORUTV_LIB") else \
+    Path(__file__).resolve().parent / LIB_NAME
 
 OK, ERR_SHAPE, ERR_NONFINITE, ERR_CUDA, ERR_COMM, ERR_CONVERGENCE, ERR_ARG, ERR_NOMEM, ERR_IO = range(9)
 EXACT_D, APPROX_D = 0, 1

@@ -26,6 +26,7 @@
 #include "common.cuh"
 #include "gemm.cuh"
 #include "qrcp_reg.cuh"
+#include "dual_sketch.cuh"
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
@@ -1703,6 +1704,25 @@ void tsr(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, i
   const GemmPlan zplan = plan_gemm(h, n, l, m, true);
   double* ws2 = nullptr;
   if (feed && zplan.splits > 1) ar.add(&ws2, (size_t)zplan.splits * n * round_up(l, 2) + 16);
+  // resident A, l <= 8, many row sub-blocks: both sketches from ONE pass over
+  // A (dual_sketch.cuh, the reference's fused_sketch sketch.py:160-163); the
+  // z partials per panel cost <= ~8 % of A's bytes.  Knobs: CORUTV_DUAL_OFF=1
+  // (two sweeps), CORUTV_DUAL_MIN_SUBS (the sub-block threshold, tests).
+  const int msubs = (int)((m + dual::BM - 1) / dual::BM);
+  const int dual_ctas = std::min<int>(h->num_sms, msubs);
+  const int dual_ppc = (msubs + dual_ctas * dual::NMS - 1) / (dual_ctas * dual::NMS);  // panels per CTA
+  const int dual_panels = dual_ctas * dual_ppc;
+  bool use_dual = false;
+  {
+    const char* off = std::getenv("CORUTV_DUAL_OFF");
+    const char* ms = std::getenv("CORUTV_DUAL_MIN_SUBS");
+    const int min_subs = ms ? std::atoi(ms) : 2 * h->num_sms;
+    use_dual = !feed && !(off && off[0] == '1') && l <= dual::ZW && msubs >= min_subs &&
+               n >= (int64_t)dual::BK * dual::KT && m < (int64_t)INT32_MAX && n < (int64_t)INT32_MAX &&
+               (ms != nullptr || (double)dual_panels * dual::ZW <= 0.10 * (double)m);
+  }
+  double* zpart = nullptr;
+  if (use_dual) ar.add(&zpart, (size_t)dual_panels * n * dual::ZW);
   ar.commit();
   Feeder fd{h, feed, m, n, lda};
   if (feed) {
@@ -1743,6 +1763,24 @@ void tsr(corutv_handle* h, const double* a, int64_t m, int64_t n, int64_t lda, i
     }
     if (ws2) finalize_splits(h, zplan, n, l, ws2, Z, ldp, nullptr, 0);
     else run_gemm(h, true, n, l, m, A, ldA, Phi, ldp, Z, ldp, nullptr, 0, ws);
+  } else if (use_dual) {
+    TagScope ts(h, 1);
+    const CUtensorMap ma = make_map(h, A, n, m, ldA, dual::BM);
+    const CUtensorMap mp = make_map(h, PsiT, n, l, ldn, dual::ZW);
+    const CUtensorMap mf = make_map(h, Phi, l, m, ldp, dual::BM);
+    {
+      ProfScope ps(h, h->tag, 4.0 * m * n * (double)l);
+      set_smem(h, dual::dual_sketch_kernel, dual::SMEM);
+      dual::dual_sketch_kernel<<<dual_ctas, dual::THREADS, dual::SMEM, h->stream>>>(
+          ma, mp, mf, m, n, msubs, dual_panels, dual_ppc, Y, ldp, zpart, flag,
+          std::getenv("CORUTV_DUAL_DBG") ? std::atoi(std::getenv("CORUTV_DUAL_DBG")) : 0);
+      CK_LAUNCH();
+    }
+    int nb, tb;
+    launch_grid_1d(n * l, &nb, &tb);
+    aux::splitk_finalize_kernel<<<nb, tb, 0, h->stream>>>(zpart, dual_panels, n * dual::ZW, n, l, dual::ZW, Z, ldp,
+                                                          nullptr, 0);
+    CK_LAUNCH();
   } else {
     TagScope ts(h, 1);
     run_gemm(h, false, m, l, n, A, ldA, PsiT, ldn, Y, ldp, nullptr, 0, ws, flag);  // y = A psi
