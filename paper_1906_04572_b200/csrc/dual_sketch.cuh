@@ -31,7 +31,7 @@
 #include "common.cuh"
 
 #ifndef DUAL_SMAX
-#define DUAL_SMAX 10  // ring depth cap (a build knob for the bytes-in-flight experiment)
+#define DUAL_SMAX 6  // ring depth cap (a build knob: the depth sweep of profiles/r02_dual_sketch.txt)
 #endif
 
 namespace dual {
@@ -49,7 +49,10 @@ constexpr int SY_BYTES = NMS * BM * ZW * 8;   // 32 KB
 constexpr int ZRED_BYTES = 4 * ZT * 2 * 3 * 32 * 16;  // quarters 1..3 of every tile of a column block: 24 KB
 constexpr int FIXED = 2 * PHI_BYTES + SY_BYTES + ZRED_BYTES + 256;
 constexpr int S_FIT = (225 * 1024 - 1024 - FIXED) / (A_BYTES + P_BYTES);
+// measured on the kernel alone (8.6 GB, l = 8): S = 3: 2.91 ms, 4: 2.28, 5: 2.65, 6: 2.31, 7: 2.56 --
+// a step takes two tiles, and an even ring keeps each step's slot pair fixed
 constexpr int S = S_FIT > DUAL_SMAX ? DUAL_SMAX : S_FIT;
+static_assert(S >= 3, "a step issues two tiles while two are being consumed");
 constexpr int SMEM = 1024 + S * (A_BYTES + P_BYTES) + FIXED;
 
 // Producer cursor: the next tile of the CTA's stream

@@ -1,0 +1,12 @@
+#!/bin/bash
+# dual sketch (16 warps): ring depth 7 vs 4 on the kernel alone, with and without the products
+mkdir -p gpurun_out
+O=gpurun_out/r27_dual.txt
+: > $O
+for lib in "" paper_1906_04572_b200/libcorutv_b200_s4.so; do
+  for d in 0 3; do
+    echo "--- lib=$lib dbg=$d" >> $O
+    CORUTV_LIB=$lib CORUTV_DUAL_DBG=$d timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:dual_sketch -c 2 python tools/tsr_ncu_target.py 2>&1 | grep -E "duration" >> $O
+  done
+done
+cat $O
