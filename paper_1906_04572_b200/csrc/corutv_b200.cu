@@ -66,6 +66,7 @@ struct corutv_handle {
   unsigned char* tails = nullptr;
   int tails_cap = 0;
   cudaEvent_t est_ev = nullptr;  // spectral norm: readiness of the async estimate
+  cudaEvent_t qr_ev = nullptr, z_ev = nullptr;  // spectral norm, deferred CholeskyQR on the side stream
   cudaEvent_t switch_ev = nullptr;  // orders a new stream after the old one (set_stream)
   int64_t m_global = 0;        // row-sharded mode: global rows stated by the host (0 = ask)
   ncclComm_t nccl = nullptr;   // native data plane (corutv_nccl_init / corutv_set_nccl)
@@ -2002,11 +2003,24 @@ void spectral_norm_fused(corutv_handle* h, const double* A, int64_t ldA, int64_t
   // before lambda_max); z = A' w is all-reduced before the replicated QR
   const bool sharded = is_sharded(h);
   Arena ar(h);
-  double *vT, *v, *w, *wT = nullptr, *ws, *gpart, *gpart2, *lam;
+  // Deferred CholeskyQR (single GPU): the next w = A v sweep reads the RAW
+  // z = A' w (finalize_kernel<2>: split-K sum + Gram partials only) while the
+  // QR chain -- first factor, apply + second factor -- runs on the side
+  // stream into its own buffer; finalize_kernel<0> then applies the product
+  // of the steps' R^-1 to the sweep's result (A (z R^-1) = (A z) R^-1).  The
+  // two factor tails and the apply launch (~50 us of a 420 us iteration)
+  // leave the critical path.  A/B knob: CORUTV_SNORM_DEFER=0.
+  static const bool defer_off = [] {
+    const char* e = std::getenv("CORUTV_SNORM_DEFER");
+    return e && e[0] == '0';
+  }();
+  const bool defer = !sharded && !defer_off;
+  double *vT, *v, *w, *wT = nullptr, *ws, *gpart, *gpart2, *lam, *vq = nullptr;
   sn::QrState* qst;
   sn::WState* wst;
   ar.add(&vT, (size_t)b * ldnp);
   ar.add(&v, (size_t)np * ldb2);
+  if (defer) ar.add(&vq, (size_t)np * ldb2);
   ar.add(&w, (size_t)mp * ldb2);
   if (!tall) ar.add(&wT, (size_t)b * ldmp);
   ar.add(&ws, std::max(gemm_ws_elems(h, m, b, n), gemm_ws_elems(h, n, b, m)) + 16);
@@ -2034,6 +2048,22 @@ void spectral_norm_fused(corutv_handle* h, const double* A, int64_t ldA, int64_t
     CK(cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&h->join_ev, cudaEventDisableTiming));
   }
+  // deferred mode: the side stream's QR chain must be over before the arena
+  // is released (every exit: return, fail(), SnormFallback)
+  struct SideJoin {
+    corutv_handle* h;
+    bool on;
+    bool pending = false;
+    ~SideJoin() {
+      if (on && pending) cudaStreamWaitEvent(h->stream, h->qr_ev, 0);
+    }
+  } side_join{h, defer};
+  if (defer && !h->qr_ev) {
+    CK(cudaEventCreateWithFlags(&h->qr_ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->z_ev, cudaEventDisableTiming));
+  }
+  // the QR chain's kernels run beside a sweep that fills every SM: few CTAs
+  const int gq = std::min(gz, 16);
   double prev = 0.0;
   for (int it = 0; it < max_iter; ++it) {
     GemmPlan pw{}, pz{};
@@ -2041,9 +2071,13 @@ void spectral_norm_fused(corutv_handle* h, const double* A, int64_t ldA, int64_t
     if (tall) run_gemm(h, false, m, b, n, A, ldA, vT, ldnp, nullptr, 0, nullptr, 0, ws, nullptr, nullptr, &pw);
     else run_gemm(h, true, n, b, m, A, ldA, v, ldb2, nullptr, 0, nullptr, 0, ws, nullptr, nullptr, &pw);
     if (it > 0) CK(cudaStreamWaitEvent(h->stream, h->est_ev, 0));  // gram_w is free again
+    if (defer && it > 0) {
+      CK(cudaStreamWaitEvent(h->stream, h->qr_ev, 0));  // rtot of the previous QR is complete
+      side_join.pending = false;
+    }
     sn::finalize_kernel<0><<<gw, sn::THREADS, 0, h->stream>>>(ws, pw.splits, mp * ldw, ldw, mp, b, w, ldb2, wT, ldmp,
                                                              gpart, gpart2, wst->tickets, gram_w, qst, 0.0, 0.0,
-                                                             it > 0 ? 1 : 0);
+                                                             it > 0 ? (defer ? 2 : 1) : 0);
     CK_LAUNCH();
     if (sharded) allreduce(h, gram_w, (int64_t)sn::B * sn::B);
     CK(cudaEventRecord(h->fork_ev, h->stream));
@@ -2063,19 +2097,42 @@ void spectral_norm_fused(corutv_handle* h, const double* A, int64_t ldA, int64_t
     } else {
       if (tall) run_gemm(h, true, n, b, m, A, ldA, w, ldb2, nullptr, 0, nullptr, 0, ws, nullptr, nullptr, &pz);
       else run_gemm(h, false, m, b, n, A, ldA, wT, ldmp, nullptr, 0, nullptr, 0, ws, nullptr, nullptr, &pz);
-      sn::finalize_kernel<1><<<gz, sn::THREADS, 0, h->stream>>>(ws, pz.splits, np * ldw, ldw, np, b, v, ldb2, vT,
-                                                               ldnp, gpart, gpart2, qst->tickets, nullptr, qst, coeff,
-                                                               kKappaPlain, 0);
+      if (defer)
+        sn::finalize_kernel<2><<<gz, sn::THREADS, 0, h->stream>>>(ws, pz.splits, np * ldw, ldw, np, b, v, ldb2, vT,
+                                                                 ldnp, gpart, gpart2, qst->tickets, nullptr, qst,
+                                                                 coeff, kKappaPlain, 0);
+      else
+        sn::finalize_kernel<1><<<gz, sn::THREADS, 0, h->stream>>>(ws, pz.splits, np * ldw, ldw, np, b, v, ldb2, vT,
+                                                                 ldnp, gpart, gpart2, qst->tickets, nullptr, qst,
+                                                                 coeff, kKappaPlain, 0);
     }
     CK_LAUNCH();
-    // typically: apply R1 + factor 2 (final: the next finalize applies it), no-op
-    for (int s = 0; s < kApply; ++s) {
-      sn::apply_kernel<<<gz, sn::THREADS, 0, h->stream>>>(v, ldb2, vT, ldnp, np, b, gpart, gpart2, qst, coeff,
-                                                          kKappaPlain, s == kApply - 1 ? 1 : 0);
+    if (defer) {
+      // side stream: factor 1 | apply R1^-1 (v -> vq) + Gram + factor 2 | (a
+      // further step if the rule asks for one), rtot = the product
+      CK(cudaEventRecord(h->z_ev, h->stream));
+      CK(cudaStreamWaitEvent(h->side, h->z_ev, 0));
+      sn::reduce_factor_kernel<<<1, sn::THREADS, 0, h->side>>>(gpart, gz, b, qst, coeff, kKappaPlain);
       CK_LAUNCH();
+      for (int s = 0; s < kApply; ++s) {
+        sn::apply_kernel<<<gq, sn::THREADS, 0, h->side>>>(s == 0 ? v : vq, vq, ldb2, nullptr, 0, np, b, gpart, gpart2,
+                                                         qst, coeff, kKappaPlain, s == kApply - 1 ? 1 : 0, 1);
+        CK_LAUNCH();
+      }
+      CK(cudaMemcpyAsync(st_pinned + 2 * (it & 1), &qst->status, sizeof(int), cudaMemcpyDeviceToHost, h->side));
+      CK(cudaEventRecord(h->qr_ev, h->side));
+      side_join.pending = true;
+    } else {
+      // typically: apply R1 + factor 2 (final: the next finalize applies it), no-op
+      for (int s = 0; s < kApply; ++s) {
+        sn::apply_kernel<<<gz, sn::THREADS, 0, h->stream>>>(v, v, ldb2, vT, ldnp, np, b, gpart, gpart2, qst, coeff,
+                                                            kKappaPlain, s == kApply - 1 ? 1 : 0, 0);
+        CK_LAUNCH();
+      }
     }
     // status of this iteration's QR, read with the next estimate
-    CK(cudaMemcpyAsync(st_pinned + 2 * (it & 1), &qst->status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    if (!defer)
+      CK(cudaMemcpyAsync(st_pinned + 2 * (it & 1), &qst->status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaEventSynchronize(h->est_ev));
     if (it > 0) {
       const int qs = st_pinned[2 * ((it - 1) & 1)];
@@ -2516,6 +2573,8 @@ void corutv_destroy(corutv_handle* h) {
   if (h->staging) cudaFreeHost(h->staging);
   if (h->tails) cudaFreeHost(h->tails);
   if (h->est_ev) cudaEventDestroy(h->est_ev);
+  if (h->qr_ev) cudaEventDestroy(h->qr_ev);
+  if (h->z_ev) cudaEventDestroy(h->z_ev);
   if (h->switch_ev) cudaEventDestroy(h->switch_ev);
   if (h->scal_dev) cudaFree(h->scal_dev);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);

@@ -29,6 +29,7 @@ constexpr int B = 32;  // register tile (b <= 32, padded)
 
 struct QrState {
   double rinv[B * B];     // R^-1 of the pending step, [k][c] (upper)
+  double rtot[B * B];     // deferred mode: the product of every step's R^-1 so far (x_raw rtot = Q)
   double kappa;
   int plain;              // consecutive unshifted steps
   int finish;             // the pending apply is the last one
@@ -402,6 +403,64 @@ __device__ bool last_cta_reduce(const double* part, double* part2, int b, unsign
   return true;
 }
 
+// Deferred mode (spectral_norm_fused): the sweep after a CholeskyQR reads the
+// un-normalised rows, and the product of all the steps' R^-1 is applied to
+// its result instead (A (x R1^-1 R2^-1) = (A x) R1^-1 R2^-1), so the QR
+// chain runs beside the sweep.  After a factor step stored st->rinv:
+// rtot <- rinv (first step) or rtot rinv.  Called by the whole CTA that ran
+// factor_step; tmp: smem B x B.
+__device__ void compose_rtot(QrState* st, int first, double* tmp) {
+  __syncthreads();  // st->rinv written by this CTA's threads
+  for (int e = threadIdx.x; e < B * B; e += THREADS) tmp[e] = first ? 0.0 : st->rtot[e];
+  __syncthreads();
+  for (int e = threadIdx.x; e < B * B; e += THREADS) {
+    const int k = e / B, c = e % B;
+    double v;
+    if (first) {
+      v = st->rinv[e];
+    } else {
+      v = 0.0;
+      for (int j = k; j <= c; ++j) v = fma(tmp[k * B + j], st->rinv[j * B + c], v);  // upper x upper
+    }
+    st->rtot[e] = v;
+  }
+  __syncthreads();
+}
+
+// last_cta_reduce's sums (groups of GS partials in slot order, then the
+// groups in order: the same floating-point sequence) by ONE CTA, for a Gram
+// whose partials a previous launch left in `part`.
+__device__ void single_cta_reduce(const double* part, int b, int count, double* Gs) {
+  constexpr int bb = B * B;
+  const int nu = b * (b + 1) / 2;
+  const int ngroups = (count + GS - 1) / GS;
+  for (int u = threadIdx.x; u < nu; u += THREADS) {
+    int i, j;
+    upper_ij(u, b, &i, &j);
+    const int idx = i * B + j;
+    double total = 0.0;
+    for (int g = 0; g < ngroups; ++g) {
+      const int gsize = min(GS, count - g * GS);
+      double v[GS];
+#pragma unroll
+      for (int c = 0; c < GS; ++c) v[c] = c < gsize ? __ldcg(part + (int64_t)(g * GS + c) * bb + idx) : 0.0;
+      double sum = 0.0;
+#pragma unroll
+      for (int c = 0; c < GS; ++c) sum += v[c];
+      if (ngroups == 1) total = sum;
+      else total += sum;
+    }
+    Gs[idx] = total;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < bb; e += THREADS) {
+    const int i = e / B, j = e % B;
+    if (i >= b || j >= b) Gs[e] = 0.0;
+    else if (i > j) Gs[e] = Gs[j * B + i];
+  }
+  __syncthreads();
+}
+
 // rows [r0, r1) of this CTA (contiguous chunks)
 __device__ __forceinline__ void cta_rows(int64_t rows, int64_t* r0, int64_t* r1) {
   const int64_t chunk = (rows + gridDim.x - 1) / gridDim.x;
@@ -567,7 +626,9 @@ __device__ __forceinline__ void finalize_rows(RowSmem& sm, const double* __restr
 
 __device__ __forceinline__ void load_pending_rinv(RowSmem& sm, const QrState* st, int use_pending) {
   for (int e = threadIdx.x; e < B * B; e += THREADS)
-    sm.Ri[(e / B) * (B + 1) + e % B] = use_pending ? __ldcg(st->rinv + e) : ((e / B == e % B) ? 1.0 : 0.0);
+    sm.Ri[(e / B) * (B + 1) + e % B] = use_pending == 2 ? __ldcg(st->rtot + e)
+                                       : use_pending  ? __ldcg(st->rinv + e)
+                                                      : ((e / B == e % B) ? 1.0 : 0.0);
 }
 
 __device__ __forceinline__ void reset_qr_state(QrState* st) {
@@ -593,7 +654,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     QrState* st, double shift_coeff, double kappa_max, int use_pending) {
   __shared__ RowSmem sm;
   if (MODE == 0) load_pending_rinv(sm, st, use_pending);
-  if (MODE == 1 && blockIdx.x == 0 && threadIdx.x == 0) {
+  if (MODE >= 1 && blockIdx.x == 0 && threadIdx.x == 0) {
     reset_qr_state(st);  // visible to the later applies
     st->prof[4] = gtimer();
     st->prof[1] = 0;
@@ -604,6 +665,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   finalize_rows<MODE>(sm, ws, splits, sstride, ldw, r0, r1, b, out, ldo, outT, ldoT, acc);
   gram_store(acc, part, blockIdx.x);
+  if (MODE == 2) return;  // deferred mode: reduce_factor_kernel (side stream) takes it from here
   if (MODE == 1 && threadIdx.x == 0) atomicMax(&st->prof[5], gtimer());
   if (!last_cta_reduce(part, part2, b, tickets, sm.u.f.G, blockIdx.x, gridDim.x)) return;
   if (MODE == 0) {
@@ -639,10 +701,13 @@ __global__ void __launch_bounds__(THREADS, 1) lmax_kernel(const double* __restri
 // of the new rows and, in the last CTA, the next factor.  Returns at once
 // when the pending factor is the final one (the next finalize_kernel<0>
 // applies it) or on an error status.
+// Deferred mode (defer != 0): the rows are read from xin (the raw sketch the
+// concurrent sweep also reads; later steps pass xin == x) and written to x,
+// and the new factor is folded into st->rtot.
 __global__ void __launch_bounds__(THREADS, 1)
-    apply_kernel(double* __restrict__ x, int64_t ldx, double* __restrict__ xT, int64_t ldxT, int64_t rows, int b,
-                 double* __restrict__ part, double* __restrict__ part2, QrState* st, double shift_coeff,
-                 double kappa_max, int last_launch) {
+    apply_kernel(const double* xin, double* x, int64_t ldx, double* __restrict__ xT, int64_t ldxT, int64_t rows,
+                 int b, double* __restrict__ part, double* __restrict__ part2, QrState* st, double shift_coeff,
+                 double kappa_max, int last_launch, int defer) {
   __shared__ RowSmem sm;
   if (*((volatile int*)&st->finish) || *((volatile int*)&st->status)) return;  // uniform: earlier launches
   if (blockIdx.x == 0 && threadIdx.x == 0) st->prof[0] = gtimer();
@@ -657,7 +722,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
       const int e = threadIdx.x + q * THREADS, r = e / B, c = e % B;
-      xv[q] = (r < nr && c < b) ? x[(c0 + r) * ldx + c] : 0.0;
+      xv[q] = (r < nr && c < b) ? xin[(c0 + r) * ldx + c] : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
@@ -676,12 +741,26 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (threadIdx.x == 0) st->prof[2] = gtimer();
   factor_step(sm.u.f.G, B, b, shift_coeff, kappa_max, st, sm.u.f.W, sm.red, sm.rowj, sm.piv);
   __syncthreads();
+  if (defer) compose_rtot(st, 0, sm.u.f.G);
   if (threadIdx.x == 0) {
     st->prof[3] = gtimer();
     st->prof[5] = 0;  // the next finalize<1>'s max-stamp starts over
   }
   // the launch budget is spent and another step would be needed
   if (threadIdx.x == 0 && last_launch && !__ldcg(&st->finish) && __ldcg(&st->status) == 0) st->status = 3;
+}
+
+// Deferred mode: the first CholeskyQR factor from the Gram partials a
+// finalize_kernel<2> launch left in `part` (count slots); one CTA.
+__global__ void __launch_bounds__(THREADS, 1)
+    reduce_factor_kernel(const double* __restrict__ part, int count, int b, QrState* st, double shift_coeff,
+                         double kappa_max) {
+  __shared__ RowSmem sm;
+  single_cta_reduce(part, b, count, sm.u.f.G);
+  factor_step(sm.u.f.G, B, b, shift_coeff, kappa_max, st, sm.u.f.W, sm.red, sm.rowj, sm.piv);
+  __syncthreads();
+  // the Gram is consumed: its storage is the scratch of the composition
+  compose_rtot(st, 1, sm.u.f.G);
 }
 
 }  // namespace sn
