@@ -19,7 +19,21 @@
 #pragma once
 #include "common.cuh"
 
+#ifndef KK_RHO
+#define KK_RHO 1  // build knob: 0 restores fragment rows r8 (2-way bank conflicts on every KK LDS.128)
+#endif
+
 namespace gemm {
+
+// KK operand rows: a 128-bit shared load is served per quarter-warp
+// (fragment rows r8 in {2q, 2q+1} x the four k chunks); consecutive rows
+// would put the quarter's eight 16-byte chunks on four bank groups twice
+// (ncu: half of all shared-memory wavefronts of the sweeps were conflicts).
+// Mapping fragment row r8 to operand row q / q + 4 -- swizzle phases that
+// differ in bit 2 -- spreads them over all eight.  The accumulator
+// fragment then holds tile row kk_row(r8) and tile columns kk_col(c4, e).
+__host__ __device__ constexpr int kk_row(int r8) { return KK_RHO ? (r8 >> 1) + 4 * (r8 & 1) : r8; }
+__host__ __device__ constexpr int kk_col(int c4, int e) { return KK_RHO ? c4 + 4 * e : 2 * c4 + e; }
 
 constexpr int BM = 128;
 constexpr int BK = 16;
@@ -202,11 +216,11 @@ __device__ __forceinline__ void mainloop(const Smem& sm, const CUtensorMap* mapA
   if (!MM) {
 #pragma unroll
     for (int p = 0; p < 2; ++p) {
-      offA[p] = ((4 * p + c4) ^ r8) << 1;
+      offA[p] = ((4 * p + c4) ^ kk_row(r8)) << 1;
       offB[p] = offA[p];
     }
-    rowA = (wm * 32 + r8) * 16;
-    rowB = (wn * 8 * J + r8) * 16;
+    rowA = (wm * 32 + kk_row(r8)) * 16;
+    rowB = (wn * 8 * J + kk_row(r8)) * 16;
   } else {
 #pragma unroll
     for (int s = 0; s < 4; ++s) mmB[s] = (s + 4 * c4) * 16;
@@ -321,7 +335,7 @@ __device__ __forceinline__ void store_acc(const Acc<J>& acc, double* out, int64_
   const int r8 = lane >> 2, c4 = lane & 3;
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi) {
-    const int row = MM ? m0 + wm * 32 + 16 * (mi >> 1) + 2 * r8 + (mi & 1) : m0 + wm * 32 + mi * 8 + r8;
+    const int row = MM ? m0 + wm * 32 + 16 * (mi >> 1) + 2 * r8 + (mi & 1) : m0 + wm * 32 + mi * 8 + kk_row(r8);
     if (row >= t.M) continue;
     double* rowp = out + (int64_t)row * ldc;
 #pragma unroll
@@ -341,9 +355,11 @@ __device__ __forceinline__ void store_acc(const Acc<J>& acc, double* out, int64_
           }
         }
       } else {
-        const int col = ncol0 + nj * 8 + 2 * c4;
-        if (col < t.N) rowp[col] = acc.v[mi][nj][0];
-        if (col + 1 < t.N) rowp[col + 1] = acc.v[mi][nj][1];
+        // (MM with an odd last fragment keeps the plain column order)
+        const int c0 = ncol0 + nj * 8 + (MM ? 2 * c4 : kk_col(c4, 0));
+        const int c1 = ncol0 + nj * 8 + (MM ? 2 * c4 + 1 : kk_col(c4, 1));
+        if (c0 < t.N) rowp[c0] = acc.v[mi][nj][0];
+        if (c1 < t.N) rowp[c1] = acc.v[mi][nj][1];
       }
     }
   }
@@ -513,11 +529,12 @@ __global__ void __launch_bounds__(THREADS, MINB)
   const int r8 = lane >> 2, c4 = lane & 3;
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi) {
-    const int row = wm * 32 + mi * 8 + r8;
+    const int row = wm * 32 + mi * 8 + kk_row(r8);
 #pragma unroll
     for (int nj = 0; nj < J; ++nj) {
-      const int col = wn * 8 * J + nj * 8 + 2 * c4;
-      *reinterpret_cast<double2*>(tileL + row * LDT + col) = make_double2(acc.v[mi][nj][0], acc.v[mi][nj][1]);
+      const int col = wn * 8 * J + nj * 8;
+      tileL[row * LDT + col + kk_col(c4, 0)] = acc.v[mi][nj][0];
+      tileL[row * LDT + col + kk_col(c4, 1)] = acc.v[mi][nj][1];
     }
   }
   __syncthreads();

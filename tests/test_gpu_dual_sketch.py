@@ -129,3 +129,18 @@ def test_dual_sketch_unaligned_view(monkeypatch):
     monkeypatch.setenv("CORUTV_DUAL_OFF", "1")
     two = P.tsr_svd(a.contiguous(), cfg)
     assert float((one.sigma[:4] - two.sigma[:4]).abs().max()) <= 1e-12 * float(two.sigma[0])
+
+
+def test_dual_sketch_strided_aligned_view(monkeypatch):
+    """Columns [0, 400) of a 402-column matrix: 16-byte aligned rows with an
+    even leading dimension go to TMA as they are (no padded copy)."""
+    monkeypatch.setenv("CORUTV_DUAL_MIN_SUBS", "2")
+    big = _matrix(2300, 402, 4, 14)
+    a = big[:, :400]
+    cfg = P.SketchConfig(ell=5, seed=6)
+    one, sweeps = _a_sweeps(lambda: P.tsr_svd(a, cfg))
+    assert sweeps == 1
+    monkeypatch.setenv("CORUTV_DUAL_OFF", "1")
+    two = P.tsr_svd(a.contiguous(), cfg)
+    assert float((one.sigma[:4] - two.sigma[:4]).abs().max()) <= 1e-12 * float(two.sigma[0])
+    assert _sign_close(one.v[:, :4], two.v[:, :4], 1e-9)
