@@ -1997,7 +1997,16 @@ void spectral_norm_fused(corutv_handle* h, const double* A, int64_t ldA, int64_t
   const int64_t np = tall ? n : m, mp = tall ? m : n;
   const int64_t ldb2 = round_up(b, 16), ldnp = round_up(np, 16), ldmp = round_up(mp, 16);
   const int64_t ldw = round_up(b, 2);
-  auto ctas = [&](int64_t rows) { return (int)std::max<int64_t>(1, std::min<int64_t>(h->num_sms, (rows + 31) / 32)); };
+  // CTAs of the row kernels (finalize / apply): one per SM by default; the
+  // two-level Gram reduction takes at most GS * GS = 256 partials
+  static const int row_ctas = [] {
+    const char* e = std::getenv("CORUTV_SNORM_CTAS");  // A/B knob
+    return e ? std::atoi(e) : 0;
+  }();
+  auto ctas = [&](int64_t rows) {
+    const int64_t cap = row_ctas > 0 ? std::min<int64_t>(row_ctas, sn::GS * sn::GS) : h->num_sms;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(cap, (rows + 31) / 32));
+  };
   const int gw = ctas(std::max<int64_t>(mp, 1)), gz = ctas(np);
   // row-sharded (tall): w and its Gram are local (the Gram is all-reduced
   // before lambda_max); z = A' w is all-reduced before the replicated QR

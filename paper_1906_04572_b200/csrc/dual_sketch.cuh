@@ -4,9 +4,10 @@
 //
 // Every 128 x 16 tile of A that TMA lands in shared memory (128-byte
 // swizzle, mbarrier full/empty ring) feeds both products on the FP64 tensor
-// pipe (DMMA.884).  One CTA of sixteen warps per SM (<= 128 registers each:
-// four warps per scheduler hide the DMMA / shared-memory latencies that two
-// could not -- the 8-warp versions ran at 3.4 TB/s whatever the ring depth):
+// pipe (DMMA.884).  One CTA of sixteen warps per SM (<= 128 registers each;
+// four warps per scheduler hide a little more of the DMMA / shared-memory
+// latency than two: 8-warp versions streamed A at 3.3-3.5 TB/s, this one at
+// 3.7-3.8; profiles/r02_dual_sketch.txt has the anatomy):
 //   * y: warp w owns rows 8w .. 8w+7 of every tile: one 8-row fragment,
 //     K = the tile's 16 columns (the KK fragment reads of gemm::mainloop),
 //     accumulated in registers over the KT k-tiles of a column block and then
