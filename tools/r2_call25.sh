@@ -1,5 +1,6 @@
 #!/bin/bash
 # dual sketch: ring depth 8 vs 5 (bytes in flight) on the kernel alone
+# variant builds (not kept in the tree): nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -I include -DDUAL_SMAX=<S> -o paper_1906_04572_b200/libcorutv_b200_s<S>.so paper_1906_04572_b200/csrc/corutv_b200.cu
 mkdir -p gpurun_out
 O=gpurun_out/r25_dual.txt
 : > $O

@@ -1,5 +1,6 @@
 #!/bin/bash
 # ALM update: 3-stage TMA ring for the rank-r product (build variant) vs the 2-stage default
+# variant build: as the default build command with LR_STAGES = 3 in csrc/gemm.cuh -> libcorutv_b200_lr3.so
 mkdir -p gpurun_out
 O=gpurun_out/r34_alm.txt
 : > $O

@@ -1,5 +1,6 @@
 #!/bin/bash
 # KK operand row map (conflict-free quarter-warp LDS.128) as a variant build: correctness + A/B
+# variant build: the default build is the row-mapped one now; -DKK_RHO=0 gives the old fragment rows (then swap the two lib paths below)
 mkdir -p gpurun_out
 O=gpurun_out/r36_rho.txt
 : > $O
