@@ -12,7 +12,8 @@ columns scaled 1/sqrt(n), k = 100, p = 10 (ell = 110), q = 2 -- the config
 quoted at 1/2/4/8 B200, row-sharded across ranks (strong scaling).  The
 same line carries the RPCA ms/iter of configs[3] (C4, n = 10000) under
 "rpca" and, at N = 1, configs[0], [1] and [4] (C1, C2, C5) under
-"workloads", each with its roofline fraction.
+"workloads", each with its roofline fraction; "tsr_svd_ell8" there times tsr_svd on
+the resident C3 matrix with one pass over A against two sweeps.
 
 Inputs are synthetic (seeded, generated on the device; no dataset).  A is
 34 GB >> the 126 MB L2, so every timed step streams it from HBM (no flush
@@ -426,6 +427,38 @@ def extra_workload(torch, P, h, device, wl, steps, warmup, peak, bw):
     return out
 
 
+def tsr_record(torch, P, a, bw, ell=8, reps=3):
+    """tsr_svd(a, ell) on the device-resident matrix, one pass over A (the
+    default for ell <= 8) and two sweeps (CORUTV_DUAL_OFF=1): ms per call with
+    CUDA events on the current stream; A is far larger than L2."""
+    m, n = a.shape
+    cfg = P.SketchConfig(ell=ell, seed=3)
+    out = {"workload": "tsr_svd", "desc": f"tsr_svd (sketch.py:220-241) on the resident {m}x{n} matrix, ell={ell}",
+           "a_bytes": 8 * m * n, "l2": "inputs larger than L2"}
+    old = os.environ.get("CORUTV_DUAL_OFF")
+    try:
+        for key, off in (("one_pass", "0"), ("two_sweeps", "1")):
+            os.environ["CORUTV_DUAL_OFF"] = off
+            f = P.tsr_svd(a, cfg)  # warm-up (workspace)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                f = P.tsr_svd(a, cfg)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            out[key] = {"ms_per_call": round(ms, 3), "sigma_0": float(f.sigma[0]),
+                        "a_reads": 1 if off == "0" else 2}
+        out["hbm_frac_one_pass"] = round(8.0 * m * n / (out["one_pass"]["ms_per_call"] * 1e-3) / (bw * 1e9), 4)
+    finally:
+        if old is None:
+            os.environ.pop("CORUTV_DUAL_OFF", None)
+        else:
+            os.environ["CORUTV_DUAL_OFF"] = old
+    return out
+
+
 def main():
     args = parse()
     world, rank, local = dist_env()
@@ -538,6 +571,15 @@ def main():
     # the reference's own corutv (baseline/_ref) on the first 32768 rows of
     # the SAME A (C3: 1/4 of it, ~10-15 s on 16 cores); the full-size CPU run
     # is the reference arm (--impl reference)
+    # tsr_svd's sketches on the same resident matrix: one pass over A (l <= 8,
+    # csrc/dual_sketch.cuh, the reference's fused_sketch sketch.py:160-163)
+    # against two DMMA sweeps -- a record next to the other workloads
+    tsr = None
+    if world == 1 and not args.no_extra:
+        try:
+            tsr = tsr_record(torch, P, a, bw)
+        except Exception as exc:  # the headline line must still print
+            tsr = {"workload": "tsr_svd", "error": str(exc)[:200]}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         rows = min(m, 32768)
@@ -633,6 +675,8 @@ def main():
                                           5 if x != "c5" else 1, peak, bw)
             except Exception as exc:  # the headline line must still print
                 extra[x] = {"workload": x, "error": str(exc)[:200]}
+        if tsr is not None:
+            extra["tsr_svd_ell8"] = tsr
 
     if rank == 0:
         line = {
